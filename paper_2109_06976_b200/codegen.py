@@ -1,0 +1,756 @@
+"""CUDA code generator: one robot -> one sm_100a library of batched kernels.
+
+Replaces the reference's IR generator (`rbdgen/codegen.py:214-856`) and its
+Python interpreter (`rbdgen/interp.py`).  Where the reference unrolls the
+recursions into a barrier-phased scalar IR executed by a thread pool, this
+module unrolls them into ONE straight-line C++ function per (algorithm,
+dtype) that evaluates a whole knot point in one CUDA thread:
+
+* every model number (joint axes, origin rotations/translations, inertias,
+  gravity) is a literal in the source, so it becomes an FMA immediate /
+  constant-bank operand; structural zeros and +-1 factors fold away at
+  generation time (`_Emit.lin`), which subsumes the reference's zero-column
+  sparsity analysis (`schedule.py:117-139`) -- a gradient column that is
+  structurally zero at a frame is simply never emitted;
+* independent root trees (fixed base with several limbs: quad12 = 4 legs,
+  humanoid30 = torso tree + 2 legs) are emitted one after another; the
+  cross-tree blocks of Minv / dID / dFD are literal zeros;
+* the mass-matrix inverse is restated column-wise: the articulated-inertia
+  factorisation (U, D^-1 per frame) is computed once, then each column of
+  Minv is one backward walk up its ancestors and one forward sweep
+  (same arithmetic as `refdyn.py:128-169`, reordered so only one 6-vector
+  per frame is live);
+* gradients are emitted column-major: for each column c (of q and of qd)
+  the outward dv/da recursion, the inward df transport and, for gradFD, the
+  product -Minv * dc[:, c] are fused, so a column's temporaries die before
+  the next column starts (`refdyn.py:178-249` computes all columns at once).
+
+The batch kernel around the per-knot function (input/output staging through
+shared memory, coalesced global traffic, launch, host-buffer pipeline) lives
+in `csrc/rbd_runtime.cuh`; the C ABI is `include/rbd_b200.h`.
+"""
+
+import hashlib
+
+import numpy as np
+
+from . import spatial
+
+ALGORITHMS = ("ID", "Minv", "FD", "gradID", "gradFD")
+DTYPES = ("f32", "f64")
+
+# reference operator I/O names (rbdgen/schedule.py:208-226)
+INPUTS = {
+    "ID": ("q", "qd", "qdd"),
+    "Minv": ("q",),
+    "FD": ("q", "qd", "tau"),
+    "gradID": ("q", "qd", "qdd"),
+    "gradFD": ("q", "qd", "tau"),
+}
+
+
+def outputs(alg, n):
+    """[(name, extent)] in output_map order."""
+    return {
+        "ID": [("tau_out", n)],
+        "Minv": [("minv_out", n * n)],
+        "FD": [("qdd_out", n)],
+        "gradID": [("dq_out", n * n), ("dqd_out", n * n)],
+        "gradFD": [("dq_out", n * n), ("dqd_out", n * n), ("qdd_out", n)],
+    }[alg]
+
+
+class GenerationError(ValueError):
+    """Model outside what the generator supports (reference `codegen.py:49`)."""
+
+
+# ---------------------------------------------------------------------------
+# folded scalar expressions
+# ---------------------------------------------------------------------------
+
+class Var:
+    """Runtime value `scale * name` (scale folds into the consumer)."""
+    __slots__ = ("name", "scale")
+
+    def __init__(self, name, scale=1.0):
+        self.name = name
+        self.scale = float(scale)
+
+    def __neg__(self):
+        return Var(self.name, -self.scale)
+
+
+def neg(e):
+    if e is None:
+        return None
+    if isinstance(e, float):
+        return -e if e != 0.0 else None
+    return -e
+
+
+class _Emit:
+    """Statement emitter with constant folding.
+
+    An entry is None (structural zero), a float (generation-time constant)
+    or a Var.  `lin` folds constants, drops zero products, merges repeated
+    single terms and returns an alias instead of emitting when the result is
+    one scaled variable.
+    """
+
+    def __init__(self, dtype):
+        self.dtype = dtype
+        self.lines = []
+        self.k = 0
+        self.flops = 0  # FMA = 2, MUL/ADD = 1 (the reference's counting rule)
+
+    def lit(self, x):
+        x = float(x)
+        if self.dtype == "f64":
+            return f"{x:.17e}"
+        return f"{np.float32(x):.9e}f"
+
+    def fresh(self, hint="t"):
+        self.k += 1
+        return f"{hint}{self.k}"
+
+    def raw(self, line):
+        self.lines.append(line)
+
+    def lin(self, terms, c0=0.0, hint="t"):
+        const = float(c0)
+        singles = {}
+        order = []
+        prods = []
+        for k, x, y in terms:
+            if x is None or y is None or k == 0.0:
+                continue
+            if isinstance(x, float) and isinstance(y, float):
+                const += k * x * y
+                continue
+            if isinstance(x, float):
+                x, y = y, x
+            if isinstance(y, float):
+                if y == 0.0:
+                    continue
+                c = k * y * x.scale
+                if x.name not in singles:
+                    singles[x.name] = 0.0
+                    order.append(x.name)
+                singles[x.name] += c
+                continue
+            prods.append((k * x.scale * y.scale, x.name, y.name))
+        sing = [(nm, singles[nm]) for nm in order if singles[nm] != 0.0]
+        if not prods and not sing:
+            return const if const != 0.0 else None
+        if not prods and len(sing) == 1 and const == 0.0:
+            return Var(sing[0][0], sing[0][1])
+        acc = None
+        fl = 0
+
+        def scaled(name, c):
+            if c == 1.0:
+                return name
+            if c == -1.0:
+                return f"-{name}"
+            return f"{name} * {self.lit(c)}"
+
+        for c, a, b in prods:
+            if acc is None:
+                if c == 1.0:
+                    acc = f"{a} * {b}"
+                elif c == -1.0:
+                    acc = f"-({a} * {b})"
+                else:
+                    acc = f"({a} * {self.lit(c)}) * {b}"
+                    fl += 1
+                fl += 1
+            else:
+                if c == 1.0 or c == -1.0:
+                    acc = f"rbd_fma({'-' if c < 0 else ''}{a}, {b}, {acc})"
+                else:
+                    acc = f"rbd_fma({a} * {self.lit(c)}, {b}, {acc})"
+                    fl += 1
+                fl += 2
+        for nm, c in sing:
+            if acc is None:
+                acc = scaled(nm, c)
+                fl += 0 if abs(c) == 1.0 else 1
+            elif c == 1.0:
+                acc = f"{acc} + {nm}"
+                fl += 1
+            elif c == -1.0:
+                acc = f"{acc} - {nm}"
+                fl += 1
+            else:
+                acc = f"rbd_fma({nm}, {self.lit(c)}, {acc})"
+                fl += 2
+        if const != 0.0:
+            acc = f"{acc} + {self.lit(const)}"
+            fl += 1
+        name = self.fresh(hint)
+        self.lines.append(f"const T {name} = {acc};")
+        self.flops += fl
+        return Var(name)
+
+    def vec(self, rows, hint="t"):
+        return [self.lin(r, hint=hint) for r in rows]
+
+    def value(self, e):
+        """C expression of an entry (for stores)."""
+        if e is None:
+            return self.lit(0.0)
+        if isinstance(e, float):
+            return self.lit(e)
+        if e.scale == 1.0:
+            return e.name
+        if e.scale == -1.0:
+            return f"-{e.name}"
+        return f"{e.name} * {self.lit(e.scale)}"
+
+
+# ---------------------------------------------------------------------------
+# term builders on 6-vectors / 6x6 grids of entries
+# ---------------------------------------------------------------------------
+
+def _rows(n=6):
+    return [[] for _ in range(n)]
+
+
+def mv_t(M, v, rows=None):
+    """rows[r] += sum_c M[r][c] v[c]."""
+    rows = rows if rows is not None else _rows(len(M))
+    if v is None:
+        return rows
+    for r in range(len(M)):
+        for c in range(len(v)):
+            rows[r].append((1.0, M[r][c], v[c]))
+    return rows
+
+
+def mtv_t(M, v, rows=None):
+    """rows[r] += sum_c M[c][r] v[c]  (transpose)."""
+    rows = rows if rows is not None else _rows(len(M[0]))
+    if v is None:
+        return rows
+    for r in range(len(M[0])):
+        for c in range(len(v)):
+            rows[r].append((1.0, M[c][r], v[c]))
+    return rows
+
+
+def add_t(rows, v, k=1.0):
+    if v is None:
+        return rows
+    for r in range(len(rows)):
+        rows[r].append((k, v[r], 1.0))
+    return rows
+
+
+def _cross3(rows, off, a, b, k=1.0):
+    """rows[off:off+3] += k * (a x b)."""
+    rows[off + 0] += [(k, a[1], b[2]), (-k, a[2], b[1])]
+    rows[off + 1] += [(k, a[2], b[0]), (-k, a[0], b[2])]
+    rows[off + 2] += [(k, a[0], b[1]), (-k, a[1], b[0])]
+
+
+def mcross_t(v, m, rows=None):
+    """rows += v x m = [w x mw; w x ml + l x mw]   (crm, reference spatial.py:45)."""
+    rows = rows if rows is not None else _rows()
+    if v is None or m is None:
+        return rows
+    w, l = v[:3], v[3:]
+    _cross3(rows, 0, w, m[:3])
+    _cross3(rows, 3, w, m[3:])
+    _cross3(rows, 3, l, m[:3])
+    return rows
+
+
+def fcross_t(v, f, rows=None):
+    """rows += v x* f = [w x fn + l x fg; w x fg]   (crf = -crm^T, spatial.py:68)."""
+    rows = rows if rows is not None else _rows()
+    if v is None or f is None:
+        return rows
+    w, l = v[:3], v[3:]
+    _cross3(rows, 0, w, f[:3])
+    _cross3(rows, 0, l, f[3:])
+    _cross3(rows, 3, w, f[3:])
+    return rows
+
+
+def _const_vec(x):
+    return [float(t) if float(t) != 0.0 else None for t in x]
+
+
+def _const_mat(M):
+    return [[float(t) if float(t) != 0.0 else None for t in row] for row in M]
+
+
+def _is_zero_vec(v):
+    return v is None or all(e is None for e in v)
+
+
+# ---------------------------------------------------------------------------
+# per-robot program emission
+# ---------------------------------------------------------------------------
+
+class _Program:
+    def __init__(self, model, alg, dtype):
+        self.model = model
+        self.alg = alg
+        self.em = _Emit(dtype)
+        self.n = model.n_dof
+        self.parent = list(model.parent)
+        self.S = [_const_vec(spatial.motion_subspace(j.kind, j.axis)) for j in model.joints]
+        self.I = [_const_mat(ine.spatial()) for ine in model.inertias]
+        g = np.asarray(model.gravity, dtype=float)
+        self.a0 = _const_vec([0.0, 0.0, 0.0, -g[0], -g[1], -g[2]])
+        self.trees = []
+        for r in model.roots():
+            self.trees.append(model.subtree(r))
+        self.X = [None] * self.n
+
+    # -- inputs and joint transforms -------------------------------------------
+    def load_inputs(self, names):
+        em = self.em
+        self.inp = {}
+        for a, nm in enumerate(names):
+            ptr = ("iq", "iqd", "iu")[a]
+            vals = []
+            for i in range(self.n):
+                v = f"{nm}{i}"
+                em.raw(f"const T {v} = {ptr}[{i}];")
+                vals.append(Var(v))
+            self.inp[nm] = vals
+
+    def emit_xform(self, i):
+        """X_i = [[E, 0], [-E skew(r), E]] as an entry grid (folded)."""
+        em = self.em
+        j = self.model.joints[i]
+        E0 = np.asarray(j.origin_rotation, dtype=float).T
+        q = self.inp["q"][i]
+        if j.kind == "revolute":
+            K = spatial.skew(j.axis)
+            A = (np.eye(3) + K @ K) @ E0
+            B = K @ E0
+            C = K @ K @ E0
+            s, c = em.fresh("s"), em.fresh("c")
+            em.raw(f"T {s}, {c}; rbd_sincos({q.name}, &{s}, &{c});")
+            sv, cv = Var(s), Var(c)
+            E = [[em.lin([(-float(B[r, k]), sv, 1.0), (-float(C[r, k]), cv, 1.0)],
+                         c0=float(A[r, k]), hint="e") for k in range(3)] for r in range(3)]
+            rv = _const_vec(j.origin_translation)
+        elif j.kind == "prismatic":
+            E = _const_mat(E0)
+            w = np.asarray(j.origin_rotation, dtype=float) @ np.asarray(j.axis, dtype=float)
+            rv = [em.lin([(float(w[k]), q, 1.0)], c0=float(j.origin_translation[k]), hint="r")
+                  for k in range(3)]
+        else:
+            raise GenerationError(f"frame {i}: fixed joints must be fused before generation")
+        sk = [[None, neg(rv[2]), rv[1]], [rv[2], None, neg(rv[0])], [neg(rv[1]), rv[0], None]]
+        Xll = [[em.lin([(-1.0, E[r][k], sk[k][c]) for k in range(3)], hint="x")
+                for c in range(3)] for r in range(3)]
+        X = [[None] * 6 for _ in range(6)]
+        for r in range(3):
+            for c in range(3):
+                X[r][c] = E[r][c]
+                X[3 + r][3 + c] = E[r][c]
+                X[3 + r][c] = Xll[r][c]
+        self.X[i] = X
+
+    def xm(self, i, v, rows=None):
+        return mv_t(self.X[i], v, rows)
+
+    def xtf(self, i, f, rows=None):
+        return mtv_t(self.X[i], f, rows)
+
+    # -- RNEA (reference refdyn.py:55-88) ----------------------------------------
+    def emit_rnea(self, tree, qdd, keep=False, v_in=None):
+        """Forward v, a, f then backward f accumulation; returns per-frame dicts.
+        qdd: per-frame entry list (None entries = zero acceleration)."""
+        em = self.em
+        qd = self.inp["qd"]
+        v, a, f, Xv, Xa, vJ, Iv = {}, {}, {}, {}, {}, {}, {}
+        for i in tree:
+            p = self.parent[i]
+            vJ[i] = [em.lin([(s, qd[i], 1.0)]) if s is not None else None for s in self.S[i]]
+            if v_in is not None:
+                v[i], Xv[i] = v_in[0][i], v_in[1][i]
+            elif p < 0:
+                Xv[i] = None
+                v[i] = vJ[i]
+            else:
+                Xv[i] = em.vec(self.xm(i, v[p]), hint="v")
+                v[i] = em.vec(add_t(_rows_from(Xv[i]), vJ[i]), hint="v")
+            Xa[i] = em.vec(self.xm(i, self.a0 if p < 0 else a[p]), hint="a")
+            rows = _rows_from(Xa[i])
+            if qdd is not None and qdd[i] is not None:
+                for r in range(6):
+                    rows[r].append((1.0, qdd[i], self.S[i][r]))
+            if p >= 0:
+                mcross_t(v[i], vJ[i], rows)
+            a[i] = em.vec(rows, hint="a")
+            Iv[i] = em.vec(mv_t(self.I[i], v[i]), hint="iv")
+            f[i] = em.vec(fcross_t(v[i], Iv[i], mv_t(self.I[i], a[i])), hint="f")
+        tau = {}
+        for i in reversed(tree):
+            tau[i] = em.lin([(1.0, f[i][r], self.S[i][r]) for r in range(6)], hint="tau")
+            p = self.parent[i]
+            if p >= 0:
+                f[p] = em.vec(add_t(self.xtf(i, f[i]), f[p]), hint="f")
+        return dict(v=v, a=a, f=f, Xv=Xv, Xa=Xa, vJ=vJ, Iv=Iv, tau=tau)
+
+    # -- direct Minv (reference refdyn.py:128-169, column-wise) ------------------
+    def emit_minv(self, tree):
+        em = self.em
+        IA = {i: [row[:] for row in self.I[i]] for i in tree}
+        U, Dinv = {}, {}
+        for i in reversed(tree):
+            S = self.S[i]
+            U[i] = em.vec([[(1.0, IA[i][r][k], S[k]) for k in range(6)] for r in range(6)], hint="u")
+            D = em.lin([(1.0, U[i][k], S[k]) for k in range(6)], hint="d")
+            dn = em.fresh("dinv")
+            em.raw(f"const T {dn} = {em.lit(1.0)} / {em.value(D)};")
+            em.flops += 1
+            Dinv[i] = Var(dn)
+            p = self.parent[i]
+            if p < 0:
+                continue
+            ud = [em.lin([(1.0, U[i][c], Dinv[i])], hint="ud") for c in range(6)]
+            Ia = [[None] * 6 for _ in range(6)]
+            for r in range(6):
+                for c in range(r, 6):
+                    Ia[r][c] = em.lin([(1.0, IA[i][r][c], 1.0), (-1.0, U[i][r], ud[c])], hint="ia")
+                    Ia[c][r] = Ia[r][c]
+            # IA_p += X^T Ia X  (symmetric: upper triangle only)
+            X = self.X[i]
+            T_ = [[em.lin([(1.0, Ia[r][k], X[k][c]) for k in range(6)], hint="ix")
+                   for c in range(6)] for r in range(6)]
+            for r in range(6):
+                for c in range(r, 6):
+                    IA[p][r][c] = em.lin([(1.0, IA[p][r][c], 1.0)]
+                                         + [(1.0, X[k][r], T_[k][c]) for k in range(6)], hint="ia")
+                    IA[p][c][r] = IA[p][r][c]
+        # per column j: backward walk up the ancestors, then forward sweep
+        M = {}
+        for j in tree:
+            mb = {}
+            F = None
+            i = j
+            while i >= 0:
+                if i == j:
+                    m = Dinv[i]
+                else:
+                    sf = em.lin([(1.0, F[k], self.S[i][k]) for k in range(6)], hint="sf")
+                    m = em.lin([(-1.0, Dinv[i], sf)], hint="mb")
+                mb[i] = m
+                p = self.parent[i]
+                if p < 0:
+                    break
+                rows = _rows()
+                add_t(rows, F)
+                for r in range(6):
+                    rows[r].append((1.0, U[i][r], m))
+                F = em.vec(self.xtf(i, em.vec(rows, hint="fb")), hint="fb")
+                i = p
+            Ff = {}
+            for i in tree:
+                if i > j:
+                    break
+                p = self.parent[i]
+                if p < 0:
+                    M[(i, j)] = mb.get(i)
+                    Ff[i] = [em.lin([(s, M[(i, j)], 1.0)]) if s is not None else None for s in self.S[i]]
+                else:
+                    t = em.vec(self.xm(i, Ff[p]), hint="ft")
+                    ut = em.lin([(1.0, U[i][k], t[k]) for k in range(6)], hint="ut")
+                    M[(i, j)] = em.lin([(1.0, mb.get(i), 1.0), (-1.0, Dinv[i], ut)], hint="m")
+                    Ff[i] = em.vec(add_t([[(s, M[(i, j)], 1.0)] if s is not None else []
+                                          for s in self.S[i]], t), hint="ff")
+        return M, U, Dinv
+
+    # -- gradient of ID, column-major (reference refdyn.py:178-239) -------------
+    def emit_grad_column(self, tree, kind, col, R):
+        """dc[:, col] for kind 'q' or 'qd' given the RNEA state R (at qdd)."""
+        em = self.em
+        dv, da, df = {}, {}, {}
+        for i in tree:
+            if i < col:
+                continue  # column col is zero at frames numbered below it
+            p = self.parent[i]
+            rows = self.xm(i, dv.get(p)) if p >= 0 else _rows()
+            if i == col:
+                seed = mcross_t(R["Xv"][i], self.S[i]) if kind == "q" else \
+                    [[(s, 1.0, 1.0)] if s is not None else [] for s in self.S[i]]
+                for r in range(6):
+                    rows[r] += seed[r]
+            if i != col and p not in da:
+                continue  # frame outside col's subtree: nothing flows out
+            dvi = em.vec(rows, hint="dv")
+            rows = self.xm(i, da.get(p)) if p >= 0 else _rows()
+            mcross_t(dvi, R["vJ"][i], rows)
+            if i == col:
+                if kind == "q":
+                    mcross_t(R["Xa"][i], self.S[i], rows)
+                else:
+                    mcross_t(R["v"][i], self.S[i], rows)
+            dai = em.vec(rows, hint="da")
+            dv[i], da[i] = dvi, dai
+            Idv = em.vec(mv_t(self.I[i], dvi), hint="idv")
+            rows = mv_t(self.I[i], dai)
+            fcross_t(R["v"][i], Idv, rows)
+            fcross_t(dvi, R["Iv"][i], rows)
+            df[i] = em.vec(rows, hint="df")
+        dc = {}
+        for i in reversed(tree):
+            fi = df.get(i)
+            if fi is not None:
+                dc[i] = em.lin([(1.0, fi[r], self.S[i][r]) for r in range(6)], hint="dc")
+            p = self.parent[i]
+            if p < 0:
+                continue
+            rows = _rows()
+            if fi is not None:
+                self.xtf(i, fi, rows)
+            if kind == "q" and i == col:
+                add_t(rows, R["xcf"][i])
+            if all(not r for r in rows):
+                continue
+            add_t(rows, df.get(p))
+            df[p] = em.vec(rows, hint="df")
+        return dc
+
+    def emit_xcf(self, tree, R):
+        """X_i^T (S_i x* f_i): the q-derivative of the inward force transport
+        (reference refdyn.py:237)."""
+        em = self.em
+        R["xcf"] = {}
+        for i in tree:
+            if self.parent[i] < 0:
+                continue
+            sf = em.vec(fcross_t(self.S[i], R["f"][i]), hint="sf")
+            R["xcf"][i] = em.vec(self.xtf(i, sf), hint="xcf")
+
+    # -- drivers -------------------------------------------------------------------
+    def store(self, slot, idx, e):
+        self.em.raw(f"{slot}[{idx}] = {self.em.value(e)};")
+
+    def run(self):
+        alg, n, em = self.alg, self.n, self.em
+        self.load_inputs(INPUTS[alg])
+        for i in range(n):
+            self.emit_xform(i)
+        stored = set()
+        for tree in self.trees:
+            if alg == "ID":
+                R = self.emit_rnea(tree, self.inp["qdd"])
+                for i in tree:
+                    self.store("o0", i, R["tau"][i])
+            elif alg == "Minv":
+                M, _, _ = self.emit_minv(tree)
+                for i in tree:
+                    for j in tree:
+                        self.store("o0", i * n + j, M[(min(i, j), max(i, j))])
+                        stored.add(i * n + j)
+            elif alg == "FD":
+                qdd = self._fd(tree)[0]
+                for i in tree:
+                    self.store("o0", i, qdd[i])
+            elif alg == "gradID":
+                R = self.emit_rnea(tree, self.inp["qdd"])
+                self.emit_xcf(tree, R)
+                for o, kind in (("o0", "q"), ("o1", "qd")):
+                    for c in tree:
+                        dc = self.emit_grad_column(tree, kind, c, R)
+                        for i in tree:
+                            self.store(o, i * n + c, dc.get(i))
+                            stored.add(i * n + c)
+            elif alg == "gradFD":
+                qdd, M, R0 = self._fd(tree)
+                for i in tree:
+                    self.store("o2", i, qdd[i])
+                R = self.emit_rnea(tree, qdd, v_in=(R0["v"], R0["Xv"]))
+                self.emit_xcf(tree, R)
+                for o, kind in (("o0", "q"), ("o1", "qd")):
+                    for c in tree:
+                        dc = self.emit_grad_column(tree, kind, c, R)
+                        for i in tree:
+                            terms = [(-1.0, M[(min(i, k), max(i, k))], dc.get(k)) for k in tree]
+                            self.store(o, i * n + c, em.lin(terms, hint="o"))
+                            stored.add(i * n + c)
+            else:
+                raise GenerationError(f"unsupported algorithm {alg!r}")
+        if alg in ("Minv", "gradID", "gradFD"):
+            # cross-tree blocks are structurally zero
+            for o in (("o0",) if alg == "Minv" else ("o0", "o1")):
+                for idx in range(n * n):
+                    if idx not in stored:
+                        self.store(o, idx, None)
+        return self.em
+
+    def _fd(self, tree):
+        """qdd = Minv (tau - c(q, qd)) (reference refdyn.py:172-175)."""
+        em = self.em
+        R0 = self.emit_rnea(tree, None)
+        M, _, _ = self.emit_minv(tree)
+        tau = self.inp["tau"]
+        umc = {i: em.lin([(1.0, tau[i], 1.0), (-1.0, R0["tau"][i], 1.0)], hint="umc") for i in tree}
+        qdd = {}
+        for i in tree:
+            qdd[i] = em.lin([(1.0, M[(min(i, k), max(i, k))], umc[k]) for k in tree], hint="qdd")
+        return qdd, M, R0
+
+
+def _rows_from(vec):
+    rows = _rows()
+    if vec is None:
+        return rows
+    for r in range(6):
+        if vec[r] is not None:
+            rows[r].append((1.0, vec[r], 1.0))
+    return rows
+
+
+# ---------------------------------------------------------------------------
+# source assembly
+# ---------------------------------------------------------------------------
+
+_ALG_ENUM = {"ID": 0, "Minv": 1, "FD": 2, "gradID": 3, "gradFD": 4}
+
+
+def _odd(x):
+    return x if x % 2 == 1 else x + 1
+
+
+def knots_per_block(model, alg, dtype):
+    """CTA size (knots per block).  One knot per thread; 64 keeps several
+    CTAs resident per SM at the ~128-255 registers the larger programs use."""
+    return 64
+
+
+def stage_outputs(model, alg, dtype, bk):
+    n = model.n_dof
+    ext = sum(e for _, e in outputs(alg, n))
+    es = 8 if dtype == "f64" else 4
+    return bk * _odd(ext) * es <= 64 * 1024
+
+
+def generate_knot(model, alg, dtype):
+    """(C++ body lines, flop count) of the one-knot program."""
+    em = _Program(model, alg, dtype).run()
+    return em.lines, em.flops
+
+
+def model_hash(model):
+    return hashlib.sha256(model.fingerprint().encode()).hexdigest()
+
+
+def _knot_struct(model, alg, dt):
+    n = model.n_dof
+    T = "double" if dt == "f64" else "float"
+    lines, fl = generate_knot(model, alg, dt)
+    outs = outputs(alg, n)
+    ext = [e for _, e in outs] + [0] * (3 - len(outs))
+    nin = len(INPUTS[alg])
+    bk = knots_per_block(model, alg, dt)
+    stage = stage_outputs(model, alg, dt, bk)
+    src = [
+        f"// GENERATED by paper_2109_06976_b200.codegen -- robot {model.name!r}, {alg} {dt}",
+        f"// {fl} flops per knot (FMA = 2, MUL/ADD = 1)",
+        "#pragma once",
+        '#include "rbd_runtime.cuh"',
+        f"struct Knot_{alg}_{dt} {{",
+        f"  typedef {T} T;",
+        f"  static constexpr int NDOF = {n}, NIN = {nin}, BK = {bk};",
+        f"  static constexpr int E0 = {ext[0]}, E1 = {ext[1]}, E2 = {ext[2]};",
+        f"  static constexpr int SIN = {_odd(nin * n)}, SOUT = {_odd(sum(ext))};",
+        f"  static constexpr bool STAGE = {'true' if stage else 'false'};",
+        f"  static constexpr int FLOPS = {fl};",
+        "  RBD_HD static void run(const T* __restrict__ iq, const T* __restrict__ iqd,",
+        "                         const T* __restrict__ iu, T* __restrict__ o0,",
+        "                         T* __restrict__ o1, T* __restrict__ o2) {",
+        "    (void)iqd; (void)iu; (void)o1; (void)o2;",
+    ]
+    src += ["    " + ln for ln in lines]
+    src += ["  }", "};", ""]
+    return "\n".join(src), fl, nin, ext
+
+
+def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
+    """{file name: text} of the per-robot library plus {(alg, dtype): flops}.
+
+    knots_<alg>_<dt>.h  the one-knot program (plain C++, also host-compilable)
+    k_<alg>_<dt>.cu     its batch kernel + the typed C-ABI entry rbd_<alg>_<dt>
+    main.cu             dispatch table, rbd_get_info, rbd_launch, host sessions
+    Separate translation units let nvcc/ptxas run in parallel.
+    """
+    n = model.n_dof
+    fp = model_hash(model)
+    files, flops, table = {}, {}, {}
+    for alg in algorithms:
+        for dt in dtypes:
+            T = "double" if dt == "f64" else "float"
+            text, fl, nin, ext = _knot_struct(model, alg, dt)
+            flops[(alg, dt)] = fl
+            table[(alg, dt)] = (nin, ext, 8 if dt == "f64" else 4)
+            files[f"knots_{alg}_{dt}.h"] = text
+            K = f"Knot_{alg}_{dt}"
+            files[f"k_{alg}_{dt}.cu"] = "\n".join([
+                f'#include "knots_{alg}_{dt}.h"',
+                f'extern "C" int rbd__launch_{alg}_{dt}(const void* q, const void* qd, const void* u,',
+                "                                void* o0, void* o1, void* o2, int64_t N, void* stream) {",
+                f"  return rbd_launch_kernel<{K}>(q, qd, u, o0, o1, o2, N, stream);",
+                "}",
+                f'extern "C" int rbd_{alg}_{dt}(const {T}* q, const {T}* qd, const {T}* u, {T}* o0,',
+                f"                         {T}* o1, {T}* o2, int64_t N, void* stream) {{",
+                f"  return rbd_launch_kernel<{K}>(q, qd, u, o0, o1, o2, N, stream);",
+                "}",
+                "",
+            ])
+    main = [
+        f"// GENERATED by paper_2109_06976_b200.codegen -- robot {model.name!r}, n_dof={n}",
+        f"// model fingerprint sha256 {fp}",
+        "#define RBD_MAIN_TU 1",
+        '#include "rbd_runtime.cuh"',
+        "",
+    ]
+    for (alg, dt) in table:
+        main.append(f'extern "C" int rbd__launch_{alg}_{dt}(const void*, const void*, const void*, '
+                    "void*, void*, void*, int64_t, void*);")
+    main += [
+        "",
+        "static int rbd_ndof() { return %d; }" % n,
+        "static const rbd_entry* rbd_entry_for(int alg, int dtype) {",
+        "  static const rbd_entry table[5][2] = {",
+    ]
+    for alg in ALGORITHMS:
+        row = []
+        for dt in DTYPES:
+            if (alg, dt) in table:
+                nin, ext, es = table[(alg, dt)]
+                row.append(f"{{&rbd__launch_{alg}_{dt}, {nin}, {ext[0]}, {ext[1]}, {ext[2]}, {es}}}")
+            else:
+                row.append("{nullptr, 0, 0, 0, 0, 0}")
+        main.append("    {" + ", ".join(row) + "},")
+    main += [
+        "  };",
+        "  if (alg < 0 || alg > 4 || dtype < 0 || dtype > 1) return nullptr;",
+        "  return table[alg][dtype].fn ? &table[alg][dtype] : nullptr;",
+        "}",
+        "",
+        'extern "C" int rbd_get_info(rbd_info* out) {',
+        "  if (!out) return RBD_EINVAL;",
+        "  out->abi_version = RBD_ABI_VERSION;",
+        f"  out->n_dof = {n};",
+        f"  out->n_frames = {model.n_frames};",
+        f"  out->n_trees = {len(model.roots())};",
+        f"  out->knots_per_block = {knots_per_block(model, 'gradFD', 'f64')};",
+        "  out->reserved = 0;",
+        f'  out->robot = "{model.name}";',
+        f'  out->fingerprint = "{fp}";',
+        "  return 0;",
+        "}",
+        "",
+    ]
+    files["main.cu"] = "\n".join(main)
+    files["knots_all.h"] = "\n".join(["#pragma once"] + [f'#include "knots_{a}_{d}.h"' for (a, d) in table]) + "\n"
+    return files, flops

@@ -1,0 +1,308 @@
+// rbd_runtime.cuh -- batch kernel template, launchers and the host-buffer
+// session shared by every generated per-robot library (see include/rbd_b200.h).
+//
+// A generated library defines, per (algorithm, dtype), a knot struct K with
+//   typedef T;  NDOF, NIN (1 or 3 inputs), E0/E1/E2 (per-knot output extents),
+//   BK (knots per CTA = threads per CTA), STAGE (stage outputs in smem),
+//   static void run(const T* q, const T* qd, const T* u, T* o0, T* o1, T* o2)
+// -- the straight-line, fully constant-folded program for ONE knot point.
+// This header turns it into a batched sm_100a kernel: one thread per knot, the
+// CTA's [BK x n] input slabs staged through shared memory with coalesced loads,
+// outputs staged per thread in shared memory and written back coalesced
+// (knot-major global layout, reference output_map order).
+#pragma once
+
+#if defined(__CUDACC__)
+#include <cuda_runtime.h>
+#endif
+#include <stdint.h>
+#include <math.h>
+
+#include "rbd_b200.h"
+
+#if defined(__CUDACC__)
+#define RBD_HD __device__ __forceinline__
+#else
+#define RBD_HD inline
+#endif
+
+RBD_HD void rbd_sincos(double x, double* s, double* c) {
+#if defined(__CUDA_ARCH__)
+  sincos(x, s, c);
+#else
+  *s = sin(x);
+  *c = cos(x);
+#endif
+}
+
+RBD_HD void rbd_sincos(float x, float* s, float* c) {
+#if defined(__CUDA_ARCH__)
+  sincosf(x, s, c);
+#else
+  *s = sinf(x);
+  *c = cosf(x);
+#endif
+}
+
+RBD_HD double rbd_fma(double a, double b, double c) { return fma(a, b, c); }
+RBD_HD float rbd_fma(float a, float b, float c) { return fmaf(a, b, c); }
+
+#if defined(__CUDACC__)
+
+// ---------------------------------------------------------------------------
+// batch kernel: CTA = BK knots, thread t = knot (blockIdx.x * BK + t)
+// ---------------------------------------------------------------------------
+template <class K>
+__global__ void __launch_bounds__(K::BK)
+rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __restrict__ qd,
+                 const typename K::T* __restrict__ u, typename K::T* __restrict__ o0,
+                 typename K::T* __restrict__ o1, typename K::T* __restrict__ o2, long long N) {
+  typedef typename K::T T;
+  constexpr int BK = K::BK, n = K::NDOF;
+  extern __shared__ __align__(16) unsigned char rbd_smem[];
+  T* s_in = reinterpret_cast<T*>(rbd_smem);  // [BK][SIN], SIN odd -> conflict-free rows
+  T* s_out = s_in + BK * K::SIN;             // [BK][SOUT] when staging
+  const long long base = (long long)blockIdx.x * BK;
+  const long long left = N - base;
+  const int nk = left < BK ? (int)left : BK;
+  const int tid = threadIdx.x;
+
+#pragma unroll
+  for (int a = 0; a < K::NIN; ++a) {
+    const T* src = (a == 0 ? q : (a == 1 ? qd : u)) + base * n;
+    T* dst = s_in + a * n;
+    for (int idx = tid; idx < BK * n; idx += BK) {
+      const int k = idx / n, j = idx - k * n;
+      dst[k * K::SIN + j] = (k < nk) ? __ldg(src + idx) : T(0);
+    }
+  }
+  __syncthreads();
+  const T* my = s_in + tid * K::SIN;
+
+  if constexpr (K::STAGE) {
+    T* o = s_out + tid * K::SOUT;
+    K::run(my, my + n, my + 2 * n, o, o + K::E0, o + K::E0 + K::E1);
+    __syncthreads();
+    // coalesced write-back, one output array at a time
+    {
+      T* dst = o0 + base * K::E0;
+      for (int idx = tid; idx < nk * K::E0; idx += BK) {
+        const int k = idx / K::E0, e = idx - k * K::E0;
+        __stcs(dst + idx, s_out[k * K::SOUT + e]);
+      }
+    }
+    if constexpr (K::E1 > 0) {
+      T* dst = o1 + base * K::E1;
+      for (int idx = tid; idx < nk * K::E1; idx += BK) {
+        const int k = idx / K::E1, e = idx - k * K::E1;
+        __stcs(dst + idx, s_out[k * K::SOUT + K::E0 + e]);
+      }
+    }
+    if constexpr (K::E2 > 0) {
+      T* dst = o2 + base * K::E2;
+      for (int idx = tid; idx < nk * K::E2; idx += BK) {
+        const int k = idx / K::E2, e = idx - k * K::E2;
+        __stcs(dst + idx, s_out[k * K::SOUT + K::E0 + K::E1 + e]);
+      }
+    }
+  } else {
+    if (tid < nk) {
+      const long long k = base + tid;
+      K::run(my, my + n, my + 2 * n, o0 + k * K::E0, K::E1 ? o1 + k * K::E1 : nullptr,
+             K::E2 ? o2 + k * K::E2 : nullptr);
+    }
+  }
+}
+
+template <class K>
+constexpr size_t rbd_smem_bytes() {
+  return sizeof(typename K::T) * (size_t)K::BK * (K::SIN + (K::STAGE ? K::SOUT : 0));
+}
+
+template <class K>
+static int rbd_launch_kernel(const void* q, const void* qd, const void* u, void* o0, void* o1,
+                             void* o2, int64_t N, void* stream) {
+  typedef typename K::T T;
+  if (N < 0) return RBD_EINVAL;
+  if (N == 0) return 0;
+  if (!q || (K::NIN == 3 && (!qd || !u)) || !o0 || (K::E1 > 0 && !o1) || (K::E2 > 0 && !o2))
+    return RBD_EINVAL;
+  constexpr size_t smem = rbd_smem_bytes<K>();
+  if (smem > 48 * 1024) {
+    // the opt-in is per device; remember which devices have it
+    static unsigned long long done = 0ull;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(done & (1ull << (dev & 63)))) {
+      cudaError_t e = cudaFuncSetAttribute(rbd_batch_kernel<K>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return (int)e;
+      done |= 1ull << (dev & 63);
+    }
+  }
+  const long long grid = (N + K::BK - 1) / K::BK;
+  rbd_batch_kernel<K><<<(unsigned)grid, K::BK, smem, (cudaStream_t)stream>>>(
+      (const T*)q, (const T*)qd, (const T*)u, (T*)o0, (T*)o1, (T*)o2, (long long)N);
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// dispatch table (filled by the generated file through rbd_entry_for)
+// ---------------------------------------------------------------------------
+typedef int (*rbd_launch_fn)(const void*, const void*, const void*, void*, void*, void*, int64_t,
+                             void*);
+struct rbd_entry {
+  rbd_launch_fn fn;
+  int32_t n_inputs;
+  int64_t e0, e1, e2;
+  int32_t elem;  // sizeof(T)
+};
+#if defined(RBD_MAIN_TU)
+static const rbd_entry* rbd_entry_for(int alg, int dtype);  // defined by the generated main TU
+static int rbd_ndof();                                       // defined by the generated main TU
+
+extern "C" int rbd_launch(int alg, int dtype, const void* q, const void* qd, const void* u,
+                          void* out0, void* out1, void* out2, int64_t N, void* stream) {
+  const rbd_entry* e = rbd_entry_for(alg, dtype);
+  if (!e) return RBD_EINVAL;
+  return e->fn(q, qd, u, out0, out1, out2, N, stream);
+}
+
+extern "C" int rbd_alg_extents(int alg, int32_t* n_inputs, int64_t* e0, int64_t* e1, int64_t* e2) {
+  const rbd_entry* e = rbd_entry_for(alg, RBD_F64);
+  if (!e) return RBD_EINVAL;
+  if (n_inputs) *n_inputs = e->n_inputs;
+  if (e0) *e0 = e->e0;
+  if (e1) *e1 = e->e1;
+  if (e2) *e2 = e->e2;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// host-buffer session: chunked H2D -> kernel -> D2H pipeline over `slots` streams
+// ---------------------------------------------------------------------------
+#define RBD_MAX_SLOTS 8
+struct rbd_session {
+  int device;
+  int64_t chunk;
+  int32_t slots;
+  size_t slot_bytes;
+  cudaStream_t stream[RBD_MAX_SLOTS];
+  unsigned char* dbuf[RBD_MAX_SLOTS];
+};
+
+extern "C" int rbd_session_create(int device, int64_t chunk_knots, int32_t slots,
+                                  rbd_session** out) {
+  if (!out || chunk_knots <= 0 || slots <= 0 || slots > RBD_MAX_SLOTS) return RBD_EINVAL;
+  *out = nullptr;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return (int)e;
+  // size for the largest per-knot footprint over all algorithms, fp64
+  int64_t per_knot = 0;
+  for (int a = 0; a < 5; ++a) {
+    const rbd_entry* en = rbd_entry_for(a, RBD_F64);
+    int64_t f = (int64_t)en->n_inputs * rbd_ndof() + en->e0 + en->e1 + en->e2;
+    if (f > per_knot) per_knot = f;
+  }
+  rbd_session* s = new rbd_session();
+  s->device = device;
+  s->chunk = chunk_knots;
+  s->slots = slots;
+  s->slot_bytes = (size_t)per_knot * (size_t)chunk_knots * sizeof(double) + 8 * 256;
+  for (int i = 0; i < slots; ++i) {
+    e = cudaStreamCreateWithFlags(&s->stream[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&s->dbuf[i], s->slot_bytes);
+    if (e != cudaSuccess) {
+      for (int j = 0; j <= i; ++j) {
+        if (s->dbuf[j]) cudaFree(s->dbuf[j]);
+        if (s->stream[j]) cudaStreamDestroy(s->stream[j]);
+      }
+      delete s;
+      cudaSetDevice(prev);
+      return (int)e;
+    }
+  }
+  cudaSetDevice(prev);
+  *out = s;
+  return 0;
+}
+
+extern "C" int rbd_session_destroy(rbd_session* s) {
+  if (!s) return RBD_ESESSION;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(s->device);
+  for (int i = 0; i < s->slots; ++i) {
+    cudaStreamSynchronize(s->stream[i]);
+    cudaFree(s->dbuf[i]);
+    cudaStreamDestroy(s->stream[i]);
+  }
+  cudaSetDevice(prev);
+  delete s;
+  return 0;
+}
+
+static inline size_t rbd_align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+extern "C" int rbd_run_host(rbd_session* s, int alg, int dtype, const void* q, const void* qd,
+                            const void* u, void* out0, void* out1, void* out2, int64_t N) {
+  if (!s) return RBD_ESESSION;
+  const rbd_entry* e = rbd_entry_for(alg, dtype);
+  if (!e || N < 0) return RBD_EINVAL;
+  if (N == 0) return 0;
+  const int64_t n = rbd_ndof();
+  const size_t es = (size_t)e->elem;
+  const void* hin[3] = {q, qd, u};
+  void* hout[3] = {out0, out1, out2};
+  const int64_t ext[3] = {e->e0, e->e1, e->e2};
+  for (int a = 0; a < e->n_inputs; ++a)
+    if (!hin[a]) return RBD_EINVAL;
+  for (int b = 0; b < 3; ++b)
+    if (ext[b] > 0 && !hout[b]) return RBD_EINVAL;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaError_t err = cudaSetDevice(s->device);
+  if (err != cudaSuccess) return (int)err;
+  int rc = 0;
+  for (int64_t c = 0, k0 = 0; k0 < N && rc == 0; ++c, k0 += s->chunk) {
+    const int slot = (int)(c % s->slots);
+    const int64_t nk = (N - k0) < s->chunk ? (N - k0) : s->chunk;
+    cudaStream_t st = s->stream[slot];
+    unsigned char* p = s->dbuf[slot];
+    const void* din[3] = {nullptr, nullptr, nullptr};
+    void* dout[3] = {nullptr, nullptr, nullptr};
+    for (int a = 0; a < e->n_inputs; ++a) {
+      const size_t bytes = (size_t)(nk * n) * es;
+      err = cudaMemcpyAsync(p, (const unsigned char*)hin[a] + (size_t)(k0 * n) * es, bytes,
+                            cudaMemcpyHostToDevice, st);
+      if (err != cudaSuccess) { rc = (int)err; break; }
+      din[a] = p;
+      p += rbd_align256(bytes);
+    }
+    if (rc) break;
+    for (int b = 0; b < 3; ++b) {
+      if (ext[b] == 0) continue;
+      dout[b] = p;
+      p += rbd_align256((size_t)(nk * ext[b]) * es);
+    }
+    rc = e->fn(din[0], din[1], din[2], dout[0], dout[1], dout[2], nk, (void*)st);
+    if (rc) break;
+    for (int b = 0; b < 3; ++b) {
+      if (ext[b] == 0) continue;
+      err = cudaMemcpyAsync((unsigned char*)hout[b] + (size_t)(k0 * ext[b]) * es, dout[b],
+                            (size_t)(nk * ext[b]) * es, cudaMemcpyDeviceToHost, st);
+      if (err != cudaSuccess) { rc = (int)err; break; }
+    }
+  }
+  for (int i = 0; i < s->slots; ++i) {
+    err = cudaStreamSynchronize(s->stream[i]);
+    if (err != cudaSuccess && rc == 0) rc = (int)err;
+  }
+  cudaSetDevice(prev);
+  return rc;
+}
+#endif  // RBD_MAIN_TU
+
+#endif  // __CUDACC__

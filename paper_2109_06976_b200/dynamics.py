@@ -1,0 +1,169 @@
+"""Batched drop-in for the reference dynamics API (`rbdgen/refdyn.py:91-249`).
+
+Same names, argument order and error behaviour as the reference, evaluated
+by the generated sm_100a kernels:
+
+    rnea(model, q, qd, qdd)              -> tau
+    bias_force(model, q, qd)             -> c = rnea(q, qd, 0)
+    minv_direct(model, q)                -> Minv
+    forward_dynamics(model, q, qd, tau)  -> qdd
+    rnea_grad(model, q, qd, qdd)         -> DynamicsGradients(dq, dqd)
+    fd_grad(model, q, qd, tau)           -> DynamicsGradients(dq, dqd) (+ .qdd)
+
+State arguments may be one knot `(n,)` (the reference's literal signature)
+or a batch `(N, n)`:
+
+* numpy arrays / sequences run through the host-buffer path of the C ABI
+  (`rbd_run_host`: chunked H2D -> kernel -> D2H pipeline) and return numpy;
+* CUDA torch tensors run through the device path (`rbd_<alg>_<dt>` on the
+  current torch stream, no copies, no synchronisation) and return CUDA
+  tensors.
+
+float32 inputs select the fp32 kernels, everything else fp64 (the reference
+precision); `dtype="f32"|"f64"` overrides.  Shapes other than (n,) / (N, n)
+raise ValueError as `refdyn._check_state` does (`refdyn.py:31-38`); host
+inputs containing non-finite values raise ValueError too.  `f_ext` is not an
+input of the generated kernels (nor of the reference's generated programs,
+`codegen.py` has none) and raises NotImplementedError when given.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import codegen, runtime
+
+_ALG_ID = {a: i for i, a in enumerate(codegen.ALGORITHMS)}
+
+
+@dataclass
+class DynamicsGradients:
+    """Partials of a joint-space output w.r.t. q (dq) and qd (dqd)
+    (reference `refdyn.py:23-28`); fd_grad also carries the solved qdd."""
+    dq: object
+    dqd: object
+    qdd: object = None
+
+
+def _is_torch(x):
+    return type(x).__module__.startswith("torch")
+
+
+def _resolve_dtype(arrs, dtype):
+    if dtype is not None:
+        if dtype not in ("f32", "f64"):
+            raise ValueError(f"dtype must be 'f32' or 'f64', got {dtype!r}")
+        return dtype
+    x = arrs[0]
+    if _is_torch(x):
+        import torch
+        return "f32" if x.dtype == torch.float32 else "f64"
+    return "f32" if getattr(np.asarray(x), "dtype", None) == np.float32 else "f64"
+
+
+def _shape_check(model, arrs):
+    n = model.n_dof
+    single = None
+    N = None
+    for x in arrs:
+        shp = tuple(x.shape)
+        if len(shp) == 1 and shp[0] == n:
+            s, k = True, 1
+        elif len(shp) == 2 and shp[1] == n:
+            s, k = False, shp[0]
+        else:
+            raise ValueError(f"state vector has shape {shp}, expected ({n},) or (N, {n})")
+        if single is None:
+            single, N = s, k
+        elif s != single or k != N:
+            raise ValueError("state arguments disagree in batch shape")
+    return single, N
+
+
+def _run(model, alg, args, dtype=None, device=None):
+    """Evaluate `alg` on state arguments `args` (1 or 3 arrays)."""
+    dt = _resolve_dtype(args, dtype)
+    on_device = _is_torch(args[0]) and args[0].is_cuda
+    lib = runtime.robot_library(model)
+    n = model.n_dof
+    if on_device:
+        import torch
+        tdt = torch.float32 if dt == "f32" else torch.float64
+        dev = args[0].device
+        xs = []
+        for x in args:
+            if not (_is_torch(x) and x.is_cuda and x.device == dev):
+                raise ValueError("mixing device and host state arguments")
+            xs.append(x.to(tdt).contiguous())
+        single, N = _shape_check(model, xs)
+        outs = [torch.empty((N, e), dtype=tdt, device=dev) for _, e in codegen.outputs(alg, n)]
+        with torch.cuda.device(dev):
+            stream = torch.cuda.current_stream(dev).cuda_stream
+            runtime.launch(lib, alg, dt, [x.data_ptr() for x in xs],
+                           [o.data_ptr() for o in outs], N, stream)
+    else:
+        ndt = np.float32 if dt == "f32" else np.float64
+        xs = []
+        for x in args:
+            if _is_torch(x):
+                x = x.detach().cpu().numpy()
+            xs.append(np.ascontiguousarray(np.asarray(x, dtype=ndt)))
+        single, N = _shape_check(model, xs)
+        for x in xs:
+            if not np.all(np.isfinite(x)):
+                raise ValueError("state vector contains non-finite entries")
+        outs = [np.empty((N, e), dtype=ndt) for _, e in codegen.outputs(alg, n)]
+        runtime.run_host(lib, alg, dt, xs, outs, N, device=device)
+    shaped = []
+    for (nm, e), o in zip(codegen.outputs(alg, n), outs):
+        shp = (n, n) if e == n * n else (n,)
+        shaped.append(o.reshape(shp) if single else o.reshape((N,) + shp))
+    return shaped
+
+
+def _no_fext(f_ext):
+    if f_ext is not None:
+        raise NotImplementedError("f_ext is not an input of the generated kernels")
+
+
+def rnea(model, q, qd, qdd, f_ext=None, dtype=None):
+    """Inverse dynamics (reference `refdyn.py:91-94`)."""
+    _no_fext(f_ext)
+    return _run(model, "ID", [q, qd, qdd], dtype)[0]
+
+
+def bias_force(model, q, qd, f_ext=None, dtype=None):
+    """rnea at qdd = 0 (reference `refdyn.py:97-100`)."""
+    _no_fext(f_ext)
+    if _is_torch(q):
+        import torch
+        zero = torch.zeros_like(q)
+    else:
+        zero = np.zeros_like(np.asarray(q, dtype=np.float32 if _resolve_dtype([q], dtype) == "f32" else np.float64))
+    return _run(model, "ID", [q, qd, zero], dtype)[0]
+
+
+def minv_direct(model, q, dtype=None):
+    """Direct inverse mass matrix (reference `refdyn.py:128-169`)."""
+    return _run(model, "Minv", [q], dtype)[0]
+
+
+def forward_dynamics(model, q, qd, tau, f_ext=None, dtype=None):
+    """qdd = Minv (tau - c) (reference `refdyn.py:172-175`)."""
+    _no_fext(f_ext)
+    return _run(model, "FD", [q, qd, tau], dtype)[0]
+
+
+def rnea_grad(model, q, qd, qdd, f_ext=None, dtype=None):
+    """(dtau/dq, dtau/dqd) (reference `refdyn.py:178-239`)."""
+    _no_fext(f_ext)
+    dq, dqd = _run(model, "gradID", [q, qd, qdd], dtype)
+    return DynamicsGradients(dq, dqd)
+
+
+def fd_grad(model, q, qd, tau, f_ext=None, dtype=None):
+    """(dqdd/dq, dqdd/dqd) = -Minv dID at qdd = FD(q, qd, tau)
+    (reference `refdyn.py:242-249`); the solved qdd rides along."""
+    _no_fext(f_ext)
+    dq, dqd, qdd = _run(model, "gradFD", [q, qd, tau], dtype)
+    return DynamicsGradients(dq, dqd, qdd)
