@@ -31,6 +31,7 @@ in `csrc/rbd_runtime.cuh`; the C ABI is `include/rbd_b200.h`.
 """
 
 import hashlib
+import struct
 
 import numpy as np
 
@@ -69,11 +70,11 @@ class GenerationError(ValueError):
 # ---------------------------------------------------------------------------
 
 class Var:
-    """Runtime value `scale * name` (scale folds into the consumer)."""
+    """Runtime value `scale * reg` (scale folds into the consumer)."""
     __slots__ = ("name", "scale")
 
     def __init__(self, name, scale=1.0):
-        self.name = name
+        self.name = name  # register id (int)
         self.scale = float(scale)
 
     def __neg__(self):
@@ -89,34 +90,63 @@ def neg(e):
 
 
 class _Emit:
-    """Statement emitter with constant folding.
+    """Op-list emitter with constant folding (the generator's IR).
 
     An entry is None (structural zero), a float (generation-time constant)
     or a Var.  `lin` folds constants, drops zero products, merges repeated
     single terms and returns an alias instead of emitting when the result is
-    one scaled variable.
+    one scaled register.  Ops (operands: register ids or float immediates):
+
+        ("ld", d, slot)            d = in[slot]      (per-knot input row)
+        ("sincos", s, c, slot)     s, c = sin/cos(in[slot])
+        ("fma", d, a, b, c) ("mul", d, a, b) ("add", d, a, b) ("sub", d, a, b)
+        ("neg", d, a) ("rcp", d, a)
+        ("st", k, idx, a)          out_k[idx] = a
     """
 
     def __init__(self, dtype):
         self.dtype = dtype
-        self.lines = []
-        self.k = 0
-        self.flops = 0  # FMA = 2, MUL/ADD = 1 (the reference's counting rule)
+        self.ops = []
+        self.nreg = 0
+        self.flops = 0  # FMA = 2, MUL/ADD/SUB/RCP = 1 (the reference's counting rule)
 
-    def lit(self, x):
-        x = float(x)
-        if self.dtype == "f64":
-            return f"{x:.17e}"
-        return f"{np.float32(x):.9e}f"
+    def reg(self):
+        self.nreg += 1
+        return self.nreg - 1
 
-    def fresh(self, hint="t"):
-        self.k += 1
-        return f"{hint}{self.k}"
+    def op(self, kind, *args):
+        d = self.reg()
+        self.ops.append((kind, d) + args)
+        self.flops += {"fma": 2, "mul": 1, "add": 1, "sub": 1, "rcp": 1}.get(kind, 0)
+        return d
 
-    def raw(self, line):
-        self.lines.append(line)
+    def load(self, slot):
+        return Var(self.op("ld", slot))
 
-    def lin(self, terms, c0=0.0, hint="t"):
+    def sincos(self, slot):
+        s, c = self.reg(), self.reg()
+        self.ops.append(("sincos", s, c, slot))
+        return Var(s), Var(c)
+
+    def rcp(self, e):
+        return Var(self.op("rcp", self.operand(e)))
+
+    def operand(self, e):
+        """Register id or float immediate holding the entry's value."""
+        if e is None:
+            return 0.0
+        if isinstance(e, float):
+            return e
+        if e.scale == 1.0:
+            return e.name
+        if e.scale == -1.0:
+            return self.op("neg", e.name)
+        return self.op("mul", e.name, e.scale)
+
+    def store(self, k, idx, e):
+        self.ops.append(("st", k, idx, self.operand(e)))
+
+    def lin(self, terms, c0=0.0, hint=None):
         const = float(c0)
         singles = {}
         order = []
@@ -144,68 +174,34 @@ class _Emit:
             return const if const != 0.0 else None
         if not prods and len(sing) == 1 and const == 0.0:
             return Var(sing[0][0], sing[0][1])
-        acc = None
-        fl = 0
-
-        def scaled(name, c):
-            if c == 1.0:
-                return name
-            if c == -1.0:
-                return f"-{name}"
-            return f"{name} * {self.lit(c)}"
-
+        acc = const if const != 0.0 else None
         for c, a, b in prods:
-            if acc is None:
-                if c == 1.0:
-                    acc = f"{a} * {b}"
-                elif c == -1.0:
-                    acc = f"-({a} * {b})"
-                else:
-                    acc = f"({a} * {self.lit(c)}) * {b}"
-                    fl += 1
-                fl += 1
-            else:
-                if c == 1.0 or c == -1.0:
-                    acc = f"rbd_fma({'-' if c < 0 else ''}{a}, {b}, {acc})"
-                else:
-                    acc = f"rbd_fma({a} * {self.lit(c)}, {b}, {acc})"
-                    fl += 1
-                fl += 2
+            if c == -1.0:
+                a = self.op("neg", a)
+            elif c != 1.0:
+                a = self.op("mul", a, c)
+            acc = self.op("mul", a, b) if acc is None else self.op("fma", a, b, acc)
         for nm, c in sing:
             if acc is None:
-                acc = scaled(nm, c)
-                fl += 0 if abs(c) == 1.0 else 1
+                acc = nm if c == 1.0 else (self.op("neg", nm) if c == -1.0 else self.op("mul", nm, c))
+                if acc == nm:
+                    acc = ("alias", nm)
             elif c == 1.0:
-                acc = f"{acc} + {nm}"
-                fl += 1
+                acc = self.op("add", _reg(acc), nm)
             elif c == -1.0:
-                acc = f"{acc} - {nm}"
-                fl += 1
+                acc = self.op("sub", _reg(acc), nm) if not isinstance(acc, float) else self.op("add", self.op("neg", nm), acc)
             else:
-                acc = f"rbd_fma({nm}, {self.lit(c)}, {acc})"
-                fl += 2
-        if const != 0.0:
-            acc = f"{acc} + {self.lit(const)}"
-            fl += 1
-        name = self.fresh(hint)
-        self.lines.append(f"const T {name} = {acc};")
-        self.flops += fl
-        return Var(name)
+                acc = self.op("fma", nm, c, _reg(acc))
+        if isinstance(acc, tuple):  # one unscaled single plus nothing else cannot reach here
+            acc = acc[1]
+        return Var(acc)
 
-    def vec(self, rows, hint="t"):
-        return [self.lin(r, hint=hint) for r in rows]
+    def vec(self, rows, hint=None):
+        return [self.lin(r) for r in rows]
 
-    def value(self, e):
-        """C expression of an entry (for stores)."""
-        if e is None:
-            return self.lit(0.0)
-        if isinstance(e, float):
-            return self.lit(e)
-        if e.scale == 1.0:
-            return e.name
-        if e.scale == -1.0:
-            return f"-{e.name}"
-        return f"{e.name} * {self.lit(e.scale)}"
+
+def _reg(acc):
+    return acc[1] if isinstance(acc, tuple) else acc
 
 
 # ---------------------------------------------------------------------------
@@ -311,16 +307,11 @@ class _Program:
 
     # -- inputs and joint transforms -------------------------------------------
     def load_inputs(self, names):
+        """Per-knot input row: q at slots [0, n), qd at [n, 2n), u at [2n, 3n)."""
         em = self.em
         self.inp = {}
         for a, nm in enumerate(names):
-            ptr = ("iq", "iqd", "iu")[a]
-            vals = []
-            for i in range(self.n):
-                v = f"{nm}{i}"
-                em.raw(f"const T {v} = {ptr}[{i}];")
-                vals.append(Var(v))
-            self.inp[nm] = vals
+            self.inp[nm] = [em.load(a * self.n + i) for i in range(self.n)]
 
     def emit_xform(self, i):
         """X_i = [[E, 0], [-E skew(r), E]] as an entry grid (folded)."""
@@ -333,9 +324,7 @@ class _Program:
             A = (np.eye(3) + K @ K) @ E0
             B = K @ E0
             C = K @ K @ E0
-            s, c = em.fresh("s"), em.fresh("c")
-            em.raw(f"T {s}, {c}; rbd_sincos({q.name}, &{s}, &{c});")
-            sv, cv = Var(s), Var(c)
+            sv, cv = em.sincos(i)  # q_i sits in input slot i
             E = [[em.lin([(-float(B[r, k]), sv, 1.0), (-float(C[r, k]), cv, 1.0)],
                          c0=float(A[r, k]), hint="e") for k in range(3)] for r in range(3)]
             rv = _const_vec(j.origin_translation)
@@ -408,10 +397,7 @@ class _Program:
             S = self.S[i]
             U[i] = em.vec([[(1.0, IA[i][r][k], S[k]) for k in range(6)] for r in range(6)], hint="u")
             D = em.lin([(1.0, U[i][k], S[k]) for k in range(6)], hint="d")
-            dn = em.fresh("dinv")
-            em.raw(f"const T {dn} = {em.lit(1.0)} / {em.value(D)};")
-            em.flops += 1
-            Dinv[i] = Var(dn)
+            Dinv[i] = em.rcp(D)
             p = self.parent[i]
             if p < 0:
                 continue
@@ -532,7 +518,7 @@ class _Program:
 
     # -- drivers -------------------------------------------------------------------
     def store(self, slot, idx, e):
-        self.em.raw(f"{slot}[{idx}] = {self.em.value(e)};")
+        self.em.store(int(slot[1]), idx, e)
 
     def run(self):
         alg, n, em = self.alg, self.n, self.em
@@ -635,44 +621,192 @@ def stage_outputs(model, alg, dtype, bk):
 
 
 def generate_knot(model, alg, dtype):
-    """(C++ body lines, flop count) of the one-knot program."""
-    em = _Program(model, alg, dtype).run()
-    return em.lines, em.flops
+    """The one-knot program as an op list (`_Emit`)."""
+    return _Program(model, alg, dtype).run()
+
+
+def _lit(x, dtype):
+    x = float(x)
+    return f"{x:.17e}" if dtype == "f64" else f"{np.float32(x):.9e}f"
+
+
+def _imm(x, dtype):
+    if dtype == "f64":
+        return "0d%016X" % struct.unpack(">Q", struct.pack(">d", float(x)))[0]
+    return "0f%08X" % struct.unpack(">I", struct.pack(">f", float(x)))[0]
+
+
+def cpp_body(em, n):
+    """Host C++ backend (test harness only): one statement per op."""
+    lit = lambda a: _lit(a, em.dtype) if isinstance(a, float) else f"r{a}"
+    out = []
+    for op in em.ops:
+        k = op[0]
+        if k == "ld":
+            out.append(f"const T r{op[1]} = {('iq', 'iqd', 'iu')[op[2] // n]}[{op[2] % n}];")
+        elif k == "sincos":
+            out.append(f"T r{op[1]}, r{op[2]}; rbd_sincos(iq[{op[3]}], &r{op[1]}, &r{op[2]});")
+        elif k == "fma":
+            out.append(f"const T r{op[1]} = rbd_fma({lit(op[2])}, {lit(op[3])}, {lit(op[4])});")
+        elif k in ("mul", "add", "sub"):
+            sym = {"mul": "*", "add": "+", "sub": "-"}[k]
+            out.append(f"const T r{op[1]} = {lit(op[2])} {sym} {lit(op[3])};")
+        elif k == "neg":
+            out.append(f"const T r{op[1]} = -{lit(op[2])};")
+        elif k == "rcp":
+            out.append(f"const T r{op[1]} = {_lit(1.0, em.dtype)} / {lit(op[2])};")
+        elif k == "st":
+            out.append(f"o{op[1]}[{op[2]}] = {lit(op[3])};")
+        else:
+            raise GenerationError(f"unknown op {k}")
+    return out
+
+
+def ptx_body(em, scratch_base, out_space):
+    """Device backend: the op list as PTX for one inline-asm block.
+
+    Operand %0 is the 32-bit shared address of the knot's input row (inputs,
+    then the sin/cos scratch the C++ prologue fills); %1..%3 address out0..2
+    (32-bit shared when staged, 64-bit global otherwise).  Straight-line PTX
+    goes to ptxas directly (no NVVM pass over ~10^4-10^5 statements);
+    ptxas allocates registers and schedules.  Returns (lines, sincos slots).
+    """
+    t = em.dtype
+    es = 8 if t == "f64" else 4
+    R = "%%fd" if t == "f64" else "%%f"
+    imm = lambda x: _imm(x, t)
+    nreg = em.nreg
+    consts = {}
+    lines = []
+
+    def r(a):
+        return imm(a) if isinstance(a, float) else f"{R}{a}"
+
+    def creg(x):
+        nonlocal nreg
+        if x not in consts:
+            consts[x] = nreg
+            nreg += 1
+            lines.append(f"mov.{t} {R}{consts[x]}, {imm(x)};")
+        return f"{R}{consts[x]}"
+
+    sc = []
+    for op in em.ops:
+        k = op[0]
+        if k == "ld":
+            lines.append(f"ld.shared.{t} {R}{op[1]}, [%0+{op[2] * es}];")
+        elif k == "sincos":
+            pos = scratch_base + 2 * len(sc)
+            sc.append(op[3])
+            lines.append(f"ld.shared.{t} {R}{op[1]}, [%0+{pos * es}];")
+            lines.append(f"ld.shared.{t} {R}{op[2]}, [%0+{(pos + 1) * es}];")
+        elif k == "fma":
+            a, b, c = op[2], op[3], op[4]
+            if isinstance(a, float):
+                a, b = b, a
+            lines.append(f"fma.rn.{t} {R}{op[1]}, {r(a)}, {r(b)}, {r(c)};")
+        elif k in ("mul", "add"):
+            a, b = op[2], op[3]
+            if isinstance(a, float):
+                a, b = b, a
+            lines.append(f"{k}.rn.{t} {R}{op[1]}, {r(a)}, {r(b)};")
+        elif k == "sub":
+            if isinstance(op[2], float):
+                lines.append(f"neg.{t} {R}{op[1]}, {r(op[3])};")
+                lines.append(f"add.rn.{t} {R}{op[1]}, {R}{op[1]}, {r(op[2])};")
+            else:
+                lines.append(f"sub.rn.{t} {R}{op[1]}, {r(op[2])}, {r(op[3])};")
+        elif k == "neg":
+            lines.append(f"neg.{t} {R}{op[1]}, {r(op[2])};")
+        elif k == "rcp":
+            lines.append(f"rcp.rn.{t} {R}{op[1]}, {r(op[2])};")
+        elif k == "st":
+            v = creg(op[3]) if isinstance(op[3], float) else r(op[3])
+            lines.append(f"st.{out_space}.{t} [%{1 + op[1]}+{op[2] * es}], {v};")
+        else:
+            raise GenerationError(f"unknown op {k}")
+    head = [f".reg .{t} {R}<{nreg}>;"]
+    return head + lines, sc
 
 
 def model_hash(model):
     return hashlib.sha256(model.fingerprint().encode()).hexdigest()
 
 
-def _knot_struct(model, alg, dt):
+def _layout(model, alg, dt, em):
     n = model.n_dof
-    T = "double" if dt == "f64" else "float"
-    lines, fl = generate_knot(model, alg, dt)
     outs = outputs(alg, n)
     ext = [e for _, e in outs] + [0] * (3 - len(outs))
     nin = len(INPUTS[alg])
+    nsc = sum(1 for op in em.ops if op[0] == "sincos")
     bk = knots_per_block(model, alg, dt)
     stage = stage_outputs(model, alg, dt, bk)
-    src = [
-        f"// GENERATED by paper_2109_06976_b200.codegen -- robot {model.name!r}, {alg} {dt}",
-        f"// {fl} flops per knot (FMA = 2, MUL/ADD = 1)",
-        "#pragma once",
-        '#include "rbd_runtime.cuh"',
+    return dict(n=n, ext=ext, nin=nin, nsc=nsc, bk=bk, stage=stage,
+                sin=_odd(nin * n + 2 * nsc), sout=_odd(sum(ext)))
+
+
+def _struct_head(model, alg, dt, L, fl):
+    T = "double" if dt == "f64" else "float"
+    return [
         f"struct Knot_{alg}_{dt} {{",
         f"  typedef {T} T;",
-        f"  static constexpr int NDOF = {n}, NIN = {nin}, BK = {bk};",
-        f"  static constexpr int E0 = {ext[0]}, E1 = {ext[1]}, E2 = {ext[2]};",
-        f"  static constexpr int SIN = {_odd(nin * n)}, SOUT = {_odd(sum(ext))};",
-        f"  static constexpr bool STAGE = {'true' if stage else 'false'};",
+        f"  static constexpr int NDOF = {L['n']}, NIN = {L['nin']}, BK = {L['bk']};",
+        f"  static constexpr int E0 = {L['ext'][0]}, E1 = {L['ext'][1]}, E2 = {L['ext'][2]};",
+        f"  static constexpr int SIN = {L['sin']}, SOUT = {L['sout']};",
+        f"  static constexpr bool STAGE = {'true' if L['stage'] else 'false'};",
         f"  static constexpr int FLOPS = {fl};",
-        "  RBD_HD static void run(const T* __restrict__ iq, const T* __restrict__ iqd,",
-        "                         const T* __restrict__ iu, T* __restrict__ o0,",
-        "                         T* __restrict__ o1, T* __restrict__ o2) {",
-        "    (void)iqd; (void)iu; (void)o1; (void)o2;",
     ]
-    src += ["    " + ln for ln in lines]
+
+
+def _knot_struct(model, alg, dt):
+    """Device header: C++ sin/cos prologue + the PTX body in one asm block."""
+    em = generate_knot(model, alg, dt)
+    L = _layout(model, alg, dt, em)
+    n = L["n"]
+    space = "shared" if L["stage"] else "global"
+    body, sc = ptx_body(em, L["nin"] * n, space)
+    src = [
+        f"// GENERATED by paper_2109_06976_b200.codegen -- robot {model.name!r}, {alg} {dt}",
+        f"// {em.flops} flops per knot (FMA = 2, MUL/ADD/SUB/RCP = 1); {em.nreg} SSA registers",
+        "#pragma once",
+        '#include "rbd_runtime.cuh"',
+    ] + _struct_head(model, alg, dt, L, em.flops) + [
+        "  __device__ __forceinline__ static void run_dev(T* my, T* o0, T* o1, T* o2) {",
+    ]
+    base = L["nin"] * n
+    for k, slot in enumerate(sc):
+        src.append(f"    {{ T s, c; rbd_sincos(my[{slot}], &s, &c); my[{base + 2 * k}] = s; my[{base + 2 * k + 1}] = c; }}")
+    src.append("    const unsigned a_in = (unsigned)__cvta_generic_to_shared(my);")
+    if L["stage"]:
+        src.append("    const unsigned a0 = (unsigned)__cvta_generic_to_shared(o0), "
+                   "a1 = (unsigned)__cvta_generic_to_shared(o1), a2 = (unsigned)__cvta_generic_to_shared(o2);")
+        ops = '"r"(a_in), "r"(a0), "r"(a1), "r"(a2)'
+    else:
+        ops = '"r"(a_in), "l"(o0), "l"(o1), "l"(o2)'
+    src.append('    asm volatile("{\\n\\t"')
+    for ln in body:
+        src.append(f'      "{ln}\\n\\t"')
+    src.append(f'      "}}" :: {ops} : "memory");')
     src += ["  }", "};", ""]
-    return "\n".join(src), fl, nin, ext
+    return "\n".join(src), em.flops, L
+
+
+def host_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
+    """TEST-ONLY: plain C++ one-knot programs for the host harness."""
+    files = {}
+    for alg in algorithms:
+        for dt in dtypes:
+            em = generate_knot(model, alg, dt)
+            L = _layout(model, alg, dt, em)
+            src = ["#pragma once", '#include "rbd_runtime.cuh"'] + _struct_head(model, alg, dt, L, em.flops) + [
+                "  static inline void run(const T* __restrict__ iq, const T* __restrict__ iqd,",
+                "                         const T* __restrict__ iu, T* __restrict__ o0,",
+                "                         T* __restrict__ o1, T* __restrict__ o2) {",
+                "    (void)iqd; (void)iu; (void)o1; (void)o2;",
+            ] + ["    " + ln for ln in cpp_body(em, L["n"])] + ["  }", "};", ""]
+            files[f"host_{alg}_{dt}.h"] = "\n".join(src)
+    files["host_all.h"] = "\n".join(["#pragma once"] + [f'#include "{f}"' for f in sorted(files)]) + "\n"
+    return files
 
 
 def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
@@ -689,9 +823,9 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
     for alg in algorithms:
         for dt in dtypes:
             T = "double" if dt == "f64" else "float"
-            text, fl, nin, ext = _knot_struct(model, alg, dt)
+            text, fl, L = _knot_struct(model, alg, dt)
             flops[(alg, dt)] = fl
-            table[(alg, dt)] = (nin, ext, 8 if dt == "f64" else 4)
+            table[(alg, dt)] = (L["nin"], L["ext"], 8 if dt == "f64" else 4)
             files[f"knots_{alg}_{dt}.h"] = text
             K = f"Knot_{alg}_{dt}"
             files[f"k_{alg}_{dt}.cu"] = "\n".join([
@@ -752,5 +886,4 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
         "",
     ]
     files["main.cu"] = "\n".join(main)
-    files["knots_all.h"] = "\n".join(["#pragma once"] + [f'#include "knots_{a}_{d}.h"' for (a, d) in table]) + "\n"
     return files, flops

@@ -4,8 +4,10 @@
 // A generated library defines, per (algorithm, dtype), a knot struct K with
 //   typedef T;  NDOF, NIN (1 or 3 inputs), E0/E1/E2 (per-knot output extents),
 //   BK (knots per CTA = threads per CTA), STAGE (stage outputs in smem),
-//   static void run(const T* q, const T* qd, const T* u, T* o0, T* o1, T* o2)
-// -- the straight-line, fully constant-folded program for ONE knot point.
+//   SIN/SOUT (per-knot smem row lengths, odd -> bank-conflict-free rows),
+//   __device__ static void run_dev(T* my_row, T* o0, T* o1, T* o2)
+// -- the straight-line, fully constant-folded program for ONE knot point
+// (a short C++ sin/cos prologue + one inline-PTX block).
 // This header turns it into a batched sm_100a kernel: one thread per knot, the
 // CTA's [BK x n] input slabs staged through shared memory with coalesced loads,
 // outputs staged per thread in shared memory and written back coalesced
@@ -77,11 +79,11 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
     }
   }
   __syncthreads();
-  const T* my = s_in + tid * K::SIN;
+  T* my = s_in + tid * K::SIN;  // this knot's inputs + its sin/cos scratch
 
   if constexpr (K::STAGE) {
     T* o = s_out + tid * K::SOUT;
-    K::run(my, my + n, my + 2 * n, o, o + K::E0, o + K::E0 + K::E1);
+    K::run_dev(my, o, o + K::E0, o + K::E0 + K::E1);
     __syncthreads();
     // coalesced write-back, one output array at a time
     {
@@ -108,8 +110,8 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
   } else {
     if (tid < nk) {
       const long long k = base + tid;
-      K::run(my, my + n, my + 2 * n, o0 + k * K::E0, K::E1 ? o1 + k * K::E1 : nullptr,
-             K::E2 ? o2 + k * K::E2 : nullptr);
+      K::run_dev(my, o0 + k * K::E0, K::E1 ? o1 + k * K::E1 : nullptr,
+                 K::E2 ? o2 + k * K::E2 : nullptr);
     }
   }
 }

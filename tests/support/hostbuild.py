@@ -21,13 +21,11 @@ def host_library(model, opt="-O0"):
     so = os.path.join(d, "host.so")
     if not os.path.exists(so):
         os.makedirs(d, exist_ok=True)
-        files, _ = codegen.generate_sources(model)
-        for nm, txt in files.items():
-            if nm.endswith(".h"):
-                with open(os.path.join(d, nm), "w") as fh:
-                    fh.write(txt)
+        for nm, txt in codegen.host_sources(model).items():
+            with open(os.path.join(d, nm), "w") as fh:
+                fh.write(txt)
         cmd = ["g++", opt, "-std=c++17", "-x", "c++", "-I", kernels.CSRC, "-I", kernels.INCLUDE,
-               "-I", d, '-DGEN_SRC="knots_all.h"', "-shared", "-fPIC", "-o", so + ".tmp",
+               "-I", d, '-DGEN_SRC="host_all.h"', "-shared", "-fPIC", "-o", so + ".tmp",
                os.path.join(HERE, "host_harness.cpp")]
         subprocess.run(cmd, check=True, capture_output=True)
         os.replace(so + ".tmp", so)

@@ -1,0 +1,159 @@
+"""GPU parity: the sm_100a kernels, called through the C ABI (device path via
+torch CUDA tensors, host path via numpy + rbd_run_host), against the
+reference's own outputs (golden fixtures) and the CPU oracle.
+
+Tolerances (north star): fp64 <= 1e-9 relative, fp32 <= 1e-4 relative against
+fp64 evaluation of the fp32-rounded inputs; norm-wise per knot and output
+(SURVEY §8c).  Cross-tree blocks must be exact zeros."""
+import numpy as np
+import pytest
+
+from conftest import MODELS, TOL, golden, rel_err
+from oracle import refdyn_np as R
+from paper_2109_06976_b200 import codegen, dynamics, kernels, models, program
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _dev(*xs, dt=torch.float64):
+    return [torch.as_tensor(x).to("cuda", dt) for x in xs]
+
+
+def _device_eval(m, alg, dt, q, qd, u):
+    from paper_2109_06976_b200 import runtime
+    lib = kernels.library(m)
+    tdt = torch.float64 if dt == "f64" else torch.float32
+    N = q.shape[0]
+    xs = _dev(q, qd, u, dt=tdt)
+    nin = len(codegen.INPUTS[alg])
+    outs = [torch.full((N, e), float("nan"), dtype=tdt, device="cuda") for _, e in codegen.outputs(alg, m.n_dof)]
+    runtime.launch(lib, alg, dt, [x.data_ptr() for x in xs[:nin]], [o.data_ptr() for o in outs], N,
+                   torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    return {nm: o.cpu().numpy() for (nm, _), o in zip(codegen.outputs(alg, m.n_dof), outs)}
+
+
+@pytest.mark.parametrize("name", MODELS)
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_all_algorithms_match_reference(name, dt):
+    g = golden(name)
+    m = models.load(name)
+    for alg in codegen.ALGORITHMS:
+        if dt == "f64":
+            q, qd, u = g["q"], g["qd"], g["u"]
+            refs = {nm: g[f"{alg}.{nm}"] for nm, _ in codegen.outputs(alg, m.n_dof)}
+        else:
+            q, qd, u = (g[k].astype(np.float32) for k in ("q", "qd", "u"))
+            refs = R.evaluate_batch(m, alg, q.astype(np.float64), qd.astype(np.float64), u.astype(np.float64))
+        out = _device_eval(m, alg, dt, q, qd, u)
+        for nm, v in out.items():
+            assert np.all(np.isfinite(v)), (name, alg, nm)
+            assert rel_err(v, refs[nm]) < TOL[dt], (name, alg, dt, nm, rel_err(v, refs[nm]))
+
+
+@pytest.mark.parametrize("name", ["quad12", "humanoid30"])
+def test_cross_tree_blocks_exact_zero(name):
+    g = golden(name)
+    m = models.load(name)
+    root = [m.root_of(i) for i in range(m.n_dof)]
+    mask = np.array([[root[i] != root[j] for j in range(m.n_dof)] for i in range(m.n_dof)])
+    for alg in ("Minv", "gradID", "gradFD"):
+        out = _device_eval(m, alg, "f64", g["q"], g["qd"], g["u"])
+        for nm, v in out.items():
+            if v.shape[1] == m.n_dof ** 2:
+                assert np.all(v.reshape(-1, m.n_dof, m.n_dof)[:, mask] == 0.0)
+
+
+@pytest.mark.parametrize("N", [0, 1, 63, 64, 65, 127, 1000])
+def test_ragged_batch_sizes(N):
+    m = models.load("chain7")
+    rng = np.random.default_rng(N)
+    n = m.n_dof
+    q, qd, u = rng.uniform(-np.pi, np.pi, (N, n)), rng.uniform(-1, 1, (N, n)), rng.uniform(-1, 1, (N, n))
+    out = _device_eval(m, "gradFD", "f64", q, qd, u)
+    if N == 0:
+        assert all(v.shape[0] == 0 for v in out.values())
+        return
+    ref = R.evaluate_batch(m, "gradFD", q, qd, u)
+    for nm in ref:
+        assert rel_err(out[nm], ref[nm]) < 1e-9
+
+
+def test_drop_in_api_host_and_device():
+    m = models.load("quad12")
+    g = golden("quad12")
+    # single knot (n,), numpy -> host-buffer path, reference return shapes
+    k = 3
+    tau = dynamics.rnea(m, g["q"][k], g["qd"][k], g["u"][k])
+    assert tau.shape == (12,) and rel_err(tau[None], g["ID.tau_out"][k:k + 1]) < 1e-9
+    Mi = dynamics.minv_direct(m, g["q"][k])
+    assert Mi.shape == (12, 12) and rel_err(Mi.reshape(1, -1), g["Minv.minv_out"][k:k + 1]) < 1e-9
+    gr = dynamics.fd_grad(m, g["q"], g["qd"], g["u"])
+    assert gr.dq.shape == (16, 12, 12)
+    assert rel_err(gr.dq, g["gradFD.dq_out"]) < 1e-9 and rel_err(gr.dqd, g["gradFD.dqd_out"]) < 1e-9
+    # device tensors stay on the device
+    gd = dynamics.rnea_grad(m, *_dev(g["q"], g["qd"], g["u"]))
+    assert gd.dq.is_cuda
+    assert rel_err(gd.dq.cpu().numpy(), g["gradID.dq_out"]) < 1e-9
+    qdd = dynamics.forward_dynamics(m, *_dev(g["q"], g["qd"], g["u"], dt=torch.float32))
+    assert qdd.dtype == torch.float32
+    c = dynamics.bias_force(m, g["q"], g["qd"])
+    assert np.allclose(dynamics.forward_dynamics(m, g["q"], g["qd"], c), 0.0, atol=1e-10)
+
+
+def test_operator_api_build_interpret():
+    m = models.load("chain7")
+    g = golden("chain7")
+    prog, sched, layout = program.build(m, "gradFD")
+    assert set(prog.input_map) == {"q", "qd", "tau"}
+    assert list(prog.output_map) == ["dq_out", "dqd_out", "qdd_out"]
+    out = program.interpret(prog, {"q": g["q"][0], "qd": g["qd"][0], "tau": g["u"][0]})
+    assert out["dq_out"].shape == (49,)
+    assert rel_err(out["dq_out"][None], g["gradFD.dq_out"][:1]) < 1e-9
+    with pytest.raises(program.InterpreterError):
+        program.interpret(prog, {"q": g["q"][0], "qd": g["qd"][0]})
+    with pytest.raises(program.InterpreterError):
+        program.interpret(prog, {"q": g["q"][0][:5], "qd": g["qd"][0], "tau": g["u"][0]})
+
+
+def test_errors_like_reference():
+    m = models.load("chain7")
+    with pytest.raises(ValueError):
+        dynamics.rnea(m, np.zeros(6), np.zeros(7), np.zeros(7))
+    with pytest.raises(ValueError):
+        dynamics.rnea(m, np.full(7, np.inf), np.zeros(7), np.zeros(7))
+    with pytest.raises(NotImplementedError):
+        dynamics.rnea(m, np.zeros(7), np.zeros(7), np.zeros(7), f_ext=np.zeros((7, 6)))
+
+
+@pytest.mark.parametrize("name,dt", [("chain7", "f64"), ("chain7", "f32"), ("humanoid30", "f64")])
+def test_full_size_properties(name, dt):
+    """BASELINE full size (N = 2^20): sampled knots vs the oracle plus
+    size-independent identities over the whole batch on the device:
+    ID(q, qd, FD(q, qd, tau)) = tau, FD qdd = gradFD qdd, Minv symmetric."""
+    from paper_2109_06976_b200 import runtime
+    m = models.load(name)
+    n = m.n_dof
+    N = 1 << 20 if name == "chain7" else 1 << 18
+    tdt = torch.float64 if dt == "f64" else torch.float32
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    q = (torch.rand((N, n), generator=gen, device="cuda", dtype=torch.float64) * 2 - 1) * np.pi
+    qd = torch.rand((N, n), generator=gen, device="cuda", dtype=torch.float64) * 2 - 1
+    tau = torch.rand((N, n), generator=gen, device="cuda", dtype=torch.float64) * 2 - 1
+    q, qd, tau = q.to(tdt), qd.to(tdt), tau.to(tdt)
+    g = dynamics.fd_grad(m, q, qd, tau)
+    qdd = dynamics.forward_dynamics(m, q, qd, tau)
+    tau2 = dynamics.rnea(m, q, qd, qdd)
+    Mi = dynamics.minv_direct(m, q)
+    torch.cuda.synchronize()
+    tol = 1e-9 if dt == "f64" else 2e-3
+    scale = tau.abs().amax(dim=1).clamp_min(1e-30)
+    assert float(((tau2 - tau).abs().amax(dim=1) / scale).max()) < tol
+    assert float(((g.qdd - qdd).abs().amax(dim=1) / qdd.abs().amax(dim=1).clamp_min(1e-30)).max()) < tol
+    assert float((Mi - Mi.transpose(1, 2)).abs().max()) <= (1e-12 if dt == "f64" else 1e-5) * float(Mi.abs().max())
+    idx = torch.randint(0, N, (24,), generator=gen, device="cuda").cpu().numpy()
+    qs, qds, taus = (x[idx].double().cpu().numpy() for x in (q, qd, tau))
+    ref = R.evaluate_batch(m, "gradFD", qs, qds, taus)
+    for nm, v in (("dq_out", g.dq), ("dqd_out", g.dqd), ("qdd_out", g.qdd)):
+        assert rel_err(v[idx].reshape(len(idx), -1).double().cpu().numpy(), ref[nm]) < TOL[dt]
