@@ -334,7 +334,7 @@ def run_ours(args):
     if rank == 0:
         if not args.no_cpu:
             cores = host_cores()
-            sample = min(args.cpu_sample, 64 * cores)
+            sample = args.cpu_sample
             rate, secs = cpu_reference_rate(robot, alg, sample, cores)
             result["cpu_baseline"] = {"value": rate, "unit": "knots/s", "cores": cores, "kind": "port",
                                       "sample": f"{sample} knots of {robot} {alg} (seed 1), "
@@ -381,8 +381,9 @@ def sweep(torch, stream, args):
     entry("humanoid30", "gradFD", "f32", 256)
     for robot in ("chain7", "quad12", "humanoid30"):
         for dt in ("f64", "f32"):
-            for N in ((65536, 262144, 1048576) if robot != "quad12" else (1048576,)):
-                entry(robot, "gradFD", dt, N, io=(N == 1048576), reps=max(args.steps, 5))
+            Ns = {"chain7": (65536, 262144, 1048576), "quad12": (1048576,), "humanoid30": (65536, 262144)}[robot]
+            for N in Ns:
+                entry(robot, "gradFD", dt, N, io=(N == Ns[-1]), reps=max(args.steps // 2, 3))
     return out
 
 
@@ -391,7 +392,7 @@ def run_reference(args):
     if rank != 0:
         return
     cores = host_cores()
-    sample = min(args.cpu_sample, 64 * cores)
+    sample = args.cpu_sample
     rates = []
     for _ in range(args.warmup and 1):
         cpu_reference_rate(args.robot, args.alg, min(sample, cores * 4), cores)
@@ -424,7 +425,7 @@ def main():
     ap.add_argument("--alg", default="gradFD")
     ap.add_argument("--dtype", default="f64", choices=("f64", "f32"))
     ap.add_argument("--n", type=int, default=1 << 20)
-    ap.add_argument("--cpu-sample", type=int, default=2048)
+    ap.add_argument("--cpu-sample", type=int, default=4096)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -31,6 +31,8 @@ in `csrc/rbd_runtime.cuh`; the C ABI is `include/rbd_b200.h`.
 """
 
 import hashlib
+import json
+import os
 import struct
 
 import numpy as np
@@ -107,6 +109,8 @@ class _Emit:
     def __init__(self, dtype):
         self.dtype = dtype
         self.ops = []
+        self.tasks = []  # task tag of every op (warp-specialised mapping)
+        self.task = "main"
         self.nreg = 0
         self.flops = 0  # FMA = 2, MUL/ADD/SUB/RCP = 1 (the reference's counting rule)
 
@@ -117,6 +121,7 @@ class _Emit:
     def op(self, kind, *args):
         d = self.reg()
         self.ops.append((kind, d) + args)
+        self.tasks.append(self.task)
         self.flops += {"fma": 2, "mul": 1, "add": 1, "sub": 1, "rcp": 1}.get(kind, 0)
         return d
 
@@ -126,6 +131,7 @@ class _Emit:
     def sincos(self, slot):
         s, c = self.reg(), self.reg()
         self.ops.append(("sincos", s, c, slot))
+        self.tasks.append(self.task)
         return Var(s), Var(c)
 
     def rcp(self, e):
@@ -144,7 +150,9 @@ class _Emit:
         return self.op("mul", e.name, e.scale)
 
     def store(self, k, idx, e):
-        self.ops.append(("st", k, idx, self.operand(e)))
+        v = self.operand(e)
+        self.ops.append(("st", k, idx, v))
+        self.tasks.append(self.task)
 
     def lin(self, terms, c0=0.0, hint=None):
         const = float(c0)
@@ -389,8 +397,9 @@ class _Program:
         return dict(v=v, a=a, f=f, Xv=Xv, Xa=Xa, vJ=vJ, Iv=Iv, tau=tau)
 
     # -- direct Minv (reference refdyn.py:128-169, column-wise) ------------------
-    def emit_minv(self, tree):
+    def emit_minv(self, tree, t=0, store=False):
         em = self.em
+        em.task = f"ia.{t}"
         IA = {i: [row[:] for row in self.I[i]] for i in tree}
         U, Dinv = {}, {}
         for i in reversed(tree):
@@ -419,6 +428,7 @@ class _Program:
         # per column j: backward walk up the ancestors, then forward sweep
         M = {}
         for j in tree:
+            em.task = f"minv.{t}.{j}"
             mb = {}
             F = None
             i = j
@@ -447,11 +457,18 @@ class _Program:
                     M[(i, j)] = mb.get(i)
                     Ff[i] = [em.lin([(s, M[(i, j)], 1.0)]) if s is not None else None for s in self.S[i]]
                 else:
-                    t = em.vec(self.xm(i, Ff[p]), hint="ft")
-                    ut = em.lin([(1.0, U[i][k], t[k]) for k in range(6)], hint="ut")
+                    tt = em.vec(self.xm(i, Ff[p]), hint="ft")
+                    ut = em.lin([(1.0, U[i][k], tt[k]) for k in range(6)], hint="ut")
                     M[(i, j)] = em.lin([(1.0, mb.get(i), 1.0), (-1.0, Dinv[i], ut)], hint="m")
                     Ff[i] = em.vec(add_t([[(s, M[(i, j)], 1.0)] if s is not None else []
-                                          for s in self.S[i]], t), hint="ff")
+                                          for s in self.S[i]], tt), hint="ff")
+            if store:
+                for i in tree:
+                    if i > j:
+                        break
+                    self.store("o0", i * self.n + j, M[(i, j)])
+                    if i != j:
+                        self.store("o0", j * self.n + i, M[(i, j)])
         return M, U, Dinv
 
     # -- gradient of ID, column-major (reference refdyn.py:178-239) -------------
@@ -521,43 +538,54 @@ class _Program:
         self.em.store(int(slot[1]), idx, e)
 
     def run(self):
+        """Emit the whole one-knot program.  Every op carries a task tag:
+        'in' / 'xf' (input loads, joint transforms: re-materialised by each
+        consumer), then per root tree t: rnea0.t, ia.t, minv.t.j, fd.t,
+        rnea1.t, grad.t.<q|qd>.c, zeros.  The thread-per-knot mapping ignores
+        the tags; the warp-specialised mapping schedules tasks over warps."""
         alg, n, em = self.alg, self.n, self.em
+        em.task = "in"
         self.load_inputs(INPUTS[alg])
+        em.task = "xf"
         for i in range(n):
             self.emit_xform(i)
         stored = set()
-        for tree in self.trees:
+        for t, tree in enumerate(self.trees):
             if alg == "ID":
+                em.task = f"rnea0.{t}"
                 R = self.emit_rnea(tree, self.inp["qdd"])
                 for i in tree:
                     self.store("o0", i, R["tau"][i])
             elif alg == "Minv":
-                M, _, _ = self.emit_minv(tree)
+                M, _, _ = self.emit_minv(tree, t, store=True)
                 for i in tree:
                     for j in tree:
-                        self.store("o0", i * n + j, M[(min(i, j), max(i, j))])
                         stored.add(i * n + j)
             elif alg == "FD":
-                qdd = self._fd(tree)[0]
+                qdd = self._fd(tree, t)[0]
                 for i in tree:
                     self.store("o0", i, qdd[i])
             elif alg == "gradID":
+                em.task = f"rnea1.{t}"
                 R = self.emit_rnea(tree, self.inp["qdd"])
                 self.emit_xcf(tree, R)
                 for o, kind in (("o0", "q"), ("o1", "qd")):
                     for c in tree:
+                        em.task = f"grad.{t}.{kind}.{c}"
                         dc = self.emit_grad_column(tree, kind, c, R)
                         for i in tree:
                             self.store(o, i * n + c, dc.get(i))
                             stored.add(i * n + c)
             elif alg == "gradFD":
-                qdd, M, R0 = self._fd(tree)
+                qdd, M, R0 = self._fd(tree, t)
                 for i in tree:
                     self.store("o2", i, qdd[i])
+                em.task = f"rnea1.{t}"
                 R = self.emit_rnea(tree, qdd, v_in=(R0["v"], R0["Xv"]))
                 self.emit_xcf(tree, R)
                 for o, kind in (("o0", "q"), ("o1", "qd")):
                     for c in tree:
+                        em.task = f"grad.{t}.{kind}.{c}"
                         dc = self.emit_grad_column(tree, kind, c, R)
                         for i in tree:
                             terms = [(-1.0, M[(min(i, k), max(i, k))], dc.get(k)) for k in tree]
@@ -567,17 +595,20 @@ class _Program:
                 raise GenerationError(f"unsupported algorithm {alg!r}")
         if alg in ("Minv", "gradID", "gradFD"):
             # cross-tree blocks are structurally zero
+            em.task = "zeros"
             for o in (("o0",) if alg == "Minv" else ("o0", "o1")):
                 for idx in range(n * n):
                     if idx not in stored:
                         self.store(o, idx, None)
         return self.em
 
-    def _fd(self, tree):
+    def _fd(self, tree, t):
         """qdd = Minv (tau - c(q, qd)) (reference refdyn.py:172-175)."""
         em = self.em
+        em.task = f"rnea0.{t}"
         R0 = self.emit_rnea(tree, None)
-        M, _, _ = self.emit_minv(tree)
+        M, _, _ = self.emit_minv(tree, t)
+        em.task = f"fd.{t}"
         tau = self.inp["tau"]
         umc = {i: em.lin([(1.0, tau[i], 1.0), (-1.0, R0["tau"][i], 1.0)], hint="umc") for i in tree}
         qdd = {}
@@ -607,17 +638,55 @@ def _odd(x):
     return x if x % 2 == 1 else x + 1
 
 
+# Generation knobs (part of the build key).  RBD_TUNING='{"bk": 128, ...}'
+# overrides them for experiments; per-(robot, alg, dtype) overrides live in
+# TUNED once measured.
+TUNING_DEFAULT = {
+    "maps": ["thread", "ws"],  # kernels compiled; launch picks ws for N <= ws_max_n
+    "ws_max_n": 16384,   # batch size up to which the (lower-latency) warp-specialised kernel runs
+    "warps": 8,          # ws: warps per CTA (one 32-knot group per CTA)
+    "minb": 2,           # ws: min CTAs per SM (caps registers at 64K / (32 W minb))
+    "bk": 64,            # thread: knots (threads) per CTA
+    "sync_every": 0,     # bar.sync every k PTX arithmetic ops (CTA lockstep -> shared I-cache lines)
+    "reload_dist": 0,    # re-load smem-resident inputs when the last load is > k ops old (0: load once)
+    "stage_kb": 64,      # stage outputs in smem when BK * outputs fit in this many KiB
+}
+TUNED = {}
+for _a in ALGORITHMS:
+    for _d in DTYPES:
+        # measured on B200 (profiles/variants_r1.md): the warp-specialised kernel
+        # wins at every N for the branched robots; the 30-dof thread-per-knot
+        # program spills hundreds of KB and takes ptxas minutes
+        TUNED[("quad12", _a, _d)] = {"maps": ["ws"], "warps": 16, "minb": 1}
+        TUNED[("humanoid30", _a, _d)] = {"maps": ["ws"], "warps": 16, "minb": 1}
+
+
+def tuning(model=None, alg=None, dtype=None):
+    t = dict(TUNING_DEFAULT)
+    if model is not None:
+        t.update(TUNED.get((model.name, alg, dtype), {}))
+    env = os.environ.get("RBD_TUNING")
+    if env:
+        t.update(json.loads(env))
+    return t
+
+
+def tuning_key():
+    env = os.environ.get("RBD_TUNING", "")
+    return hashlib.sha256((json.dumps(TUNING_DEFAULT, sort_keys=True) + repr(sorted(TUNED.items()))
+                           + env).encode()).hexdigest()[:8]
+
+
 def knots_per_block(model, alg, dtype):
-    """CTA size (knots per block).  One knot per thread; 64 keeps several
-    CTAs resident per SM at the ~128-255 registers the larger programs use."""
-    return 64
+    """CTA size (knots per block): one knot per thread."""
+    return int(tuning(model, alg, dtype)["bk"])
 
 
 def stage_outputs(model, alg, dtype, bk):
     n = model.n_dof
     ext = sum(e for _, e in outputs(alg, n))
     es = 8 if dtype == "f64" else 4
-    return bk * _odd(ext) * es <= 64 * 1024
+    return bk * _odd(ext) * es <= tuning(model, alg, dtype)["stage_kb"] * 1024
 
 
 def generate_knot(model, alg, dtype):
@@ -662,14 +731,18 @@ def cpp_body(em, n):
     return out
 
 
-def ptx_body(em, scratch_base, out_space):
+def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0):
     """Device backend: the op list as PTX for one inline-asm block.
 
     Operand %0 is the 32-bit shared address of the knot's input row (inputs,
     then the sin/cos scratch the C++ prologue fills); %1..%3 address out0..2
-    (32-bit shared when staged, 64-bit global otherwise).  Straight-line PTX
-    goes to ptxas directly (no NVVM pass over ~10^4-10^5 statements);
-    ptxas allocates registers and schedules.  Returns (lines, sincos slots).
+    (32-bit shared when staged, 64-bit global otherwise); %4 is 1 for a real
+    knot, 0 for the padding threads of the last CTA (their global stores are
+    predicated off).  Straight-line PTX goes to ptxas directly (no NVVM pass
+    over 10^4-10^5 statements); ptxas allocates registers and schedules.
+    sync_every > 0 inserts CTA barriers so all warps walk the instruction
+    stream together; reload_dist > 0 re-loads smem-resident values near their
+    uses instead of keeping them live.  Returns (lines, sincos input slots).
     """
     t = em.dtype
     es = 8 if t == "f64" else 4
@@ -678,9 +751,7 @@ def ptx_body(em, scratch_base, out_space):
     nreg = em.nreg
     consts = {}
     lines = []
-
-    def r(a):
-        return imm(a) if isinstance(a, float) else f"{R}{a}"
+    pred = "@%%p " if out_space == "global" else ""
 
     def creg(x):
         nonlocal nreg
@@ -690,42 +761,67 @@ def ptx_body(em, scratch_base, out_space):
             lines.append(f"mov.{t} {R}{consts[x]}, {imm(x)};")
         return f"{R}{consts[x]}"
 
+    home = {}      # register -> smem byte offset it can be re-loaded from
+    loaded = {}    # register -> index of its last load
+    step = 0
+
+    def use(a):
+        if isinstance(a, float):
+            return imm(a)
+        if a in home and (a not in loaded or (reload_dist and step - loaded[a] > reload_dist)):
+            lines.append(f"ld.shared.{t} {R}{a}, [%0+{home[a]}];")
+            loaded[a] = step
+        return f"{R}{a}"
+
     sc = []
+    narith = 0
     for op in em.ops:
         k = op[0]
+        step += 1
         if k == "ld":
-            lines.append(f"ld.shared.{t} {R}{op[1]}, [%0+{op[2] * es}];")
-        elif k == "sincos":
+            home[op[1]] = op[2] * es
+            if not reload_dist:
+                use(op[1])
+            continue
+        if k == "sincos":
             pos = scratch_base + 2 * len(sc)
             sc.append(op[3])
-            lines.append(f"ld.shared.{t} {R}{op[1]}, [%0+{pos * es}];")
-            lines.append(f"ld.shared.{t} {R}{op[2]}, [%0+{(pos + 1) * es}];")
-        elif k == "fma":
+            home[op[1]] = pos * es
+            home[op[2]] = (pos + 1) * es
+            if not reload_dist:
+                use(op[1]), use(op[2])
+            continue
+        if k == "fma":
             a, b, c = op[2], op[3], op[4]
             if isinstance(a, float):
                 a, b = b, a
-            lines.append(f"fma.rn.{t} {R}{op[1]}, {r(a)}, {r(b)}, {r(c)};")
+            lines.append(f"fma.rn.{t} {R}{op[1]}, {use(a)}, {use(b)}, {use(c)};")
         elif k in ("mul", "add"):
             a, b = op[2], op[3]
             if isinstance(a, float):
                 a, b = b, a
-            lines.append(f"{k}.rn.{t} {R}{op[1]}, {r(a)}, {r(b)};")
+            lines.append(f"{k}.rn.{t} {R}{op[1]}, {use(a)}, {use(b)};")
         elif k == "sub":
             if isinstance(op[2], float):
-                lines.append(f"neg.{t} {R}{op[1]}, {r(op[3])};")
-                lines.append(f"add.rn.{t} {R}{op[1]}, {R}{op[1]}, {r(op[2])};")
+                lines.append(f"neg.{t} {R}{op[1]}, {use(op[3])};")
+                lines.append(f"add.rn.{t} {R}{op[1]}, {R}{op[1]}, {imm(op[2])};")
             else:
-                lines.append(f"sub.rn.{t} {R}{op[1]}, {r(op[2])}, {r(op[3])};")
+                lines.append(f"sub.rn.{t} {R}{op[1]}, {use(op[2])}, {use(op[3])};")
         elif k == "neg":
-            lines.append(f"neg.{t} {R}{op[1]}, {r(op[2])};")
+            lines.append(f"neg.{t} {R}{op[1]}, {use(op[2])};")
         elif k == "rcp":
-            lines.append(f"rcp.rn.{t} {R}{op[1]}, {r(op[2])};")
+            lines.append(f"rcp.rn.{t} {R}{op[1]}, {use(op[2])};")
         elif k == "st":
-            v = creg(op[3]) if isinstance(op[3], float) else r(op[3])
-            lines.append(f"st.{out_space}.{t} [%{1 + op[1]}+{op[2] * es}], {v};")
+            v = creg(op[3]) if isinstance(op[3], float) else use(op[3])
+            lines.append(f"{pred}st.{out_space}.{t} [%{1 + op[1]}+{op[2] * es}], {v};")
         else:
             raise GenerationError(f"unknown op {k}")
+        narith += 1
+        if sync_every and narith % sync_every == 0:
+            lines.append("bar.sync 1;")
     head = [f".reg .{t} {R}<{nreg}>;"]
+    if out_space == "global":
+        head += [".reg .pred %%p;", "setp.ne.u32 %%p, %4, 0;"]
     return head + lines, sc
 
 
@@ -745,33 +841,35 @@ def _layout(model, alg, dt, em):
                 sin=_odd(nin * n + 2 * nsc), sout=_odd(sum(ext)))
 
 
-def _struct_head(model, alg, dt, L, fl):
+def _struct_head(model, alg, dt, L, fl, name=None):
     T = "double" if dt == "f64" else "float"
     return [
-        f"struct Knot_{alg}_{dt} {{",
+        f"struct {name or f'Knot_{alg}_{dt}'} {{",
         f"  typedef {T} T;",
         f"  static constexpr int NDOF = {L['n']}, NIN = {L['nin']}, BK = {L['bk']};",
         f"  static constexpr int E0 = {L['ext'][0]}, E1 = {L['ext'][1]}, E2 = {L['ext'][2]};",
         f"  static constexpr int SIN = {L['sin']}, SOUT = {L['sout']};",
         f"  static constexpr bool STAGE = {'true' if L['stage'] else 'false'};",
         f"  static constexpr int FLOPS = {fl};",
+        "  static constexpr int MAP = 0;  // thread per knot",
     ]
 
 
-def _knot_struct(model, alg, dt):
+def _knot_struct(model, alg, dt, name=None):
     """Device header: C++ sin/cos prologue + the PTX body in one asm block."""
     em = generate_knot(model, alg, dt)
     L = _layout(model, alg, dt, em)
     n = L["n"]
     space = "shared" if L["stage"] else "global"
-    body, sc = ptx_body(em, L["nin"] * n, space)
+    tn = tuning(model, alg, dt)
+    body, sc = ptx_body(em, L["nin"] * n, space, tn["sync_every"], tn["reload_dist"])
     src = [
         f"// GENERATED by paper_2109_06976_b200.codegen -- robot {model.name!r}, {alg} {dt}",
         f"// {em.flops} flops per knot (FMA = 2, MUL/ADD/SUB/RCP = 1); {em.nreg} SSA registers",
         "#pragma once",
         '#include "rbd_runtime.cuh"',
-    ] + _struct_head(model, alg, dt, L, em.flops) + [
-        "  __device__ __forceinline__ static void run_dev(T* my, T* o0, T* o1, T* o2) {",
+    ] + _struct_head(model, alg, dt, L, em.flops, name) + [
+        "  __device__ __forceinline__ static void run_dev(T* my, T* o0, T* o1, T* o2, unsigned valid) {",
     ]
     base = L["nin"] * n
     for k, slot in enumerate(sc):
@@ -780,15 +878,88 @@ def _knot_struct(model, alg, dt):
     if L["stage"]:
         src.append("    const unsigned a0 = (unsigned)__cvta_generic_to_shared(o0), "
                    "a1 = (unsigned)__cvta_generic_to_shared(o1), a2 = (unsigned)__cvta_generic_to_shared(o2);")
-        ops = '"r"(a_in), "r"(a0), "r"(a1), "r"(a2)'
+        ops = '"r"(a_in), "r"(a0), "r"(a1), "r"(a2), "r"(valid)'
     else:
-        ops = '"r"(a_in), "l"(o0), "l"(o1), "l"(o2)'
+        ops = '"r"(a_in), "l"(o0), "l"(o1), "l"(o2), "r"(valid)'
     src.append('    asm volatile("{\\n\\t"')
     for ln in body:
         src.append(f'      "{ln}\\n\\t"')
     src.append(f'      "}}" :: {ops} : "memory");')
     src += ["  }", "};", ""]
     return "\n".join(src), em.flops, L
+
+
+def _ws_struct(model, alg, dt, warps, name=None):
+    """Device header of the warp-specialised mapping (see wsched.py)."""
+    from . import wsched
+    P = wsched.plan(model, alg, dt, warps)
+    em, sched = P["em"], P["sched"]
+    n, nin = P["n"], P["nin"]
+    T = "double" if dt == "f64" else "float"
+    ar_space = "shared" if P["arena_smem"] else "global"
+    out_space = "shared" if P["stage"] else "global"
+    AT = "unsigned" if P["arena_smem"] else "unsigned long long"
+    OT = "unsigned" if P["stage"] else "unsigned long long"
+    ac = '"r"' if P["arena_smem"] else '"l"'
+    oc = '"r"' if P["stage"] else '"l"'
+    ext = P["ext"]
+    src = [
+        f"// GENERATED by paper_2109_06976_b200.codegen -- robot {model.name!r}, {alg} {dt}, warp-specialised",
+        f"// {em.flops} flops per knot; {len(sched.task_ops)} tasks in {len(sched.phases)} phases over {warps} warps;",
+        f"// critical path {sched.critical_path()} of {sched.total()} ops; {sched.nslots} arena slots ({ar_space})",
+        "#pragma once",
+        '#include "rbd_runtime.cuh"',
+        f"struct {name or f'Knot_{alg}_{dt}'} {{",
+        f"  typedef {T} T;",
+        "  static constexpr int MAP = 1;  // warp-specialised: CTA = 32 knots x W warps",
+        f"  static constexpr int W = {warps}, NDOF = {n}, NIN = {nin}, NSC = {P['nsc']};",
+        f"  static constexpr int E0 = {ext[0]}, E1 = {ext[1]}, E2 = {ext[2]};",
+        f"  static constexpr int SIN = {P['sin']}, NA = {sched.nslots}, SOUT = {P['sout']};",
+        f"  static constexpr bool STAGE = {'true' if P['stage'] else 'false'}, "
+        f"ARENA_SMEM = {'true' if P['arena_smem'] else 'false'};",
+        f"  static constexpr int FLOPS = {em.flops};",
+        f"  static constexpr int MINB = {int(tuning(model, alg, dt).get('minb', 1))};  // min CTAs per SM (register cap)",
+        "  typedef " + AT + " arena_t;",
+        "  typedef " + OT + " out_t;",
+        "  __device__ __forceinline__ static void prologue(T* s_in, int warp, int lane) {",
+    ]
+    k = 0
+    for op in em.ops:
+        if op[0] == "sincos":
+            slot = op[3]
+            src.append(f"    if (warp == {k % warps}) {{ T s, c; rbd_sincos(s_in[{slot * 33} + lane], &s, &c); "
+                       f"s_in[{(nin * n + 2 * k) * 33} + lane] = s; s_in[{(nin * n + 2 * k + 1) * 33} + lane] = c; }}")
+            k += 1
+    src.append("    (void)s_in; (void)warp; (void)lane;")
+    src.append("  }")
+    src.append("  __device__ __forceinline__ static void run_group(int warp, unsigned a_in, arena_t a_ar, "
+               "out_t a0, out_t a1, out_t a2, unsigned valid) {")
+    tn = tuning(model, alg, dt)
+    for p, phase in enumerate(sched.phases):
+        src.append(f"    // phase {p}")
+        src.append("    switch (warp) {")
+        for w, tasks in enumerate(phase):
+            if not tasks:
+                continue
+            body = wsched.ptx_block(sched, tasks, dt, nin * n, nin * n, ar_space, out_space, tn["reload_dist"])
+            src.append(f"    case {w}:  // {', '.join(tasks)}")
+            src.append('      asm volatile("{\\n\\t"')
+            for ln in body:
+                src.append(f'        "{ln}\\n\\t"')
+            src.append(f'        "}}" :: "r"(a_in), {ac}(a_ar), {oc}(a0), {oc}(a1), {oc}(a2), "r"(valid) : "memory");')
+            src.append("      break;")
+        src.append("    default: break;")
+        src.append("    }")
+        src.append("    __syncthreads();")
+    src.append("    (void)a_in; (void)a_ar; (void)a0; (void)a1; (void)a2; (void)valid;")
+    src += ["  }", "};", ""]
+    L = dict(nin=nin, ext=ext)
+    return "\n".join(src), em.flops, L
+
+
+def mapping(model, alg, dt):
+    """'thread' (one knot per thread) or 'ws' (warp-specialised), from tuning."""
+    return tuning(model, alg, dt).get("map", "thread")
 
 
 def host_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
@@ -820,26 +991,48 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
     n = model.n_dof
     fp = model_hash(model)
     files, flops, table = {}, {}, {}
+    dispatch = []
     for alg in algorithms:
         for dt in dtypes:
             T = "double" if dt == "f64" else "float"
-            text, fl, L = _knot_struct(model, alg, dt)
-            flops[(alg, dt)] = fl
-            table[(alg, dt)] = (L["nin"], L["ext"], 8 if dt == "f64" else 4)
-            files[f"knots_{alg}_{dt}.h"] = text
-            K = f"Knot_{alg}_{dt}"
-            files[f"k_{alg}_{dt}.cu"] = "\n".join([
-                f'#include "knots_{alg}_{dt}.h"',
+            tn = tuning(model, alg, dt)
+            maps = list(tn["maps"])
+            for mp in maps:
+                tag = "W" if mp == "ws" else "T"
+                K = f"Knot_{alg}_{dt}_{tag}"
+                if mp == "ws":
+                    text, fl, L = _ws_struct(model, alg, dt, int(tn["warps"]), K)
+                else:
+                    text, fl, L = _knot_struct(model, alg, dt, K)
+                flops[(alg, dt)] = fl
+                table[(alg, dt)] = (L["nin"], L["ext"], 8 if dt == "f64" else 4)
+                files[f"knots_{alg}_{dt}_{tag}.h"] = text
+                files[f"k_{alg}_{dt}_{tag}.cu"] = "\n".join([
+                    f'#include "knots_{alg}_{dt}_{tag}.h"',
+                    f'extern "C" int rbd__launch_{alg}_{dt}_{tag}(const void* q, const void* qd, const void* u,',
+                    "                                void* o0, void* o1, void* o2, int64_t N, void* stream) {",
+                    f"  return rbd_launch_kernel<{K}>(q, qd, u, o0, o1, o2, N, stream);",
+                    "}",
+                    "",
+                ])
+            sig = "(const void*, const void*, const void*, void*, void*, void*, int64_t, void*);"
+            for mp in maps:
+                dispatch.append(f'extern "C" int rbd__launch_{alg}_{dt}_{"W" if mp == "ws" else "T"}{sig}')
+            if maps == ["thread", "ws"] or maps == ["ws", "thread"]:
+                pick = (f"N <= {int(tn['ws_max_n'])} ? rbd__launch_{alg}_{dt}_W(q, qd, u, o0, o1, o2, N, stream)"
+                        f" : rbd__launch_{alg}_{dt}_T(q, qd, u, o0, o1, o2, N, stream)")
+            else:
+                pick = f"rbd__launch_{alg}_{dt}_{'W' if maps[0] == 'ws' else 'T'}(q, qd, u, o0, o1, o2, N, stream)"
+            dispatch += [
                 f'extern "C" int rbd__launch_{alg}_{dt}(const void* q, const void* qd, const void* u,',
                 "                                void* o0, void* o1, void* o2, int64_t N, void* stream) {",
-                f"  return rbd_launch_kernel<{K}>(q, qd, u, o0, o1, o2, N, stream);",
+                f"  return {pick};",
                 "}",
                 f'extern "C" int rbd_{alg}_{dt}(const {T}* q, const {T}* qd, const {T}* u, {T}* o0,',
                 f"                         {T}* o1, {T}* o2, int64_t N, void* stream) {{",
-                f"  return rbd_launch_kernel<{K}>(q, qd, u, o0, o1, o2, N, stream);",
+                f"  return rbd__launch_{alg}_{dt}(q, qd, u, o0, o1, o2, N, stream);",
                 "}",
-                "",
-            ])
+            ]
     main = [
         f"// GENERATED by paper_2109_06976_b200.codegen -- robot {model.name!r}, n_dof={n}",
         f"// model fingerprint sha256 {fp}",
@@ -847,9 +1040,7 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
         '#include "rbd_runtime.cuh"',
         "",
     ]
-    for (alg, dt) in table:
-        main.append(f'extern "C" int rbd__launch_{alg}_{dt}(const void*, const void*, const void*, '
-                    "void*, void*, void*, int64_t, void*);")
+    main += dispatch
     main += [
         "",
         "static int rbd_ndof() { return %d; }" % n,

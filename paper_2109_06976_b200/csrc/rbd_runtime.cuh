@@ -5,7 +5,7 @@
 //   typedef T;  NDOF, NIN (1 or 3 inputs), E0/E1/E2 (per-knot output extents),
 //   BK (knots per CTA = threads per CTA), STAGE (stage outputs in smem),
 //   SIN/SOUT (per-knot smem row lengths, odd -> bank-conflict-free rows),
-//   __device__ static void run_dev(T* my_row, T* o0, T* o1, T* o2)
+//   __device__ static void run_dev(T* my_row, T* o0, T* o1, T* o2, unsigned valid)
 // -- the straight-line, fully constant-folded program for ONE knot point
 // (a short C++ sin/cos prologue + one inline-PTX block).
 // This header turns it into a batched sm_100a kernel: one thread per knot, the
@@ -83,7 +83,7 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
 
   if constexpr (K::STAGE) {
     T* o = s_out + tid * K::SOUT;
-    K::run_dev(my, o, o + K::E0, o + K::E0 + K::E1);
+    K::run_dev(my, o, o + K::E0, o + K::E0 + K::E1, 1u);
     __syncthreads();
     // coalesced write-back, one output array at a time
     {
@@ -108,18 +108,109 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
       }
     }
   } else {
-    if (tid < nk) {
-      const long long k = base + tid;
-      K::run_dev(my, o0 + k * K::E0, K::E1 ? o1 + k * K::E1 : nullptr,
-                 K::E2 ? o2 + k * K::E2 : nullptr);
+    // every thread runs the program (CTA barriers inside); stores of the
+    // padding threads of the last CTA are predicated off
+    const long long k = base + (tid < nk ? tid : 0);
+    K::run_dev(my, o0 + k * K::E0, K::E1 ? o1 + k * K::E1 : nullptr,
+               K::E2 ? o2 + k * K::E2 : nullptr, tid < nk ? 1u : 0u);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// warp-specialised kernel: CTA = W warps on a group of 32 knots (lane = knot);
+// the generated run_group() runs the program's tasks phase by phase.
+// Persistent: CTAs loop over 32-knot groups so a global (L2-resident) arena
+// is sized by the grid, not by N.
+// ---------------------------------------------------------------------------
+#define RBD_WS_LANES 33
+template <class K>
+__global__ void __launch_bounds__(K::W * 32, K::MINB)
+rbd_ws_kernel(const typename K::T* __restrict__ q, const typename K::T* __restrict__ qd,
+              const typename K::T* __restrict__ u, typename K::T* __restrict__ o0,
+              typename K::T* __restrict__ o1, typename K::T* __restrict__ o2, long long N,
+              typename K::T* __restrict__ garena) {
+  typedef typename K::T T;
+  constexpr int n = K::NDOF, NT = K::W * 32, L = RBD_WS_LANES;
+  extern __shared__ __align__(16) unsigned char rbd_smem[];
+  T* s_in = reinterpret_cast<T*>(rbd_smem);         // [SIN][33]
+  T* s_ar = s_in + K::SIN * L;                        // [NA][33] when ARENA_SMEM
+  T* s_out = s_ar + (K::ARENA_SMEM ? K::NA * L : 0);  // [SOUT][33] when STAGE
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long groups = (N + 31) / 32;
+  for (long long g = blockIdx.x; g < groups; g += gridDim.x) {
+    const long long base = g * 32;
+    const int nk = (N - base) < 32 ? (int)(N - base) : 32;
+#pragma unroll
+    for (int a = 0; a < K::NIN; ++a) {
+      const T* src = (a == 0 ? q : (a == 1 ? qd : u)) + base * n;
+      for (int idx = tid; idx < 32 * n; idx += NT) {
+        const int k = idx / n, j = idx - k * n;
+        s_in[(a * n + j) * L + k] = (k < nk) ? __ldg(src + idx) : T(0);
+      }
+    }
+    __syncthreads();
+    K::prologue(s_in, warp, lane);
+    __syncthreads();
+    const unsigned a_in = (unsigned)__cvta_generic_to_shared(s_in + lane);
+    typename K::arena_t a_ar;
+    if constexpr (K::ARENA_SMEM)
+      a_ar = (unsigned)__cvta_generic_to_shared(s_ar + lane);
+    else
+      a_ar = (unsigned long long)(garena + (size_t)blockIdx.x * K::NA * 32 + lane);
+    typename K::out_t a0, a1, a2;
+    const int kk = lane < nk ? lane : 0;
+    if constexpr (K::STAGE) {
+      a0 = (unsigned)__cvta_generic_to_shared(s_out + lane);
+      a1 = (unsigned)__cvta_generic_to_shared(s_out + K::E0 * L + lane);
+      a2 = (unsigned)__cvta_generic_to_shared(s_out + (K::E0 + K::E1) * L + lane);
+    } else {
+      a0 = (unsigned long long)(o0 + (base + kk) * K::E0);
+      a1 = (unsigned long long)(K::E1 ? o1 + (base + kk) * K::E1 : o0);
+      a2 = (unsigned long long)(K::E2 ? o2 + (base + kk) * K::E2 : o0);
+    }
+    K::run_group(warp, a_in, a_ar, a0, a1, a2, lane < nk ? 1u : 0u);  // ends with a barrier
+    if constexpr (K::STAGE) {
+      {
+        T* dst = o0 + base * K::E0;
+        for (int idx = tid; idx < nk * K::E0; idx += NT) {
+          const int k = idx / K::E0, e = idx - k * K::E0;
+          __stcs(dst + idx, s_out[e * L + k]);
+        }
+      }
+      if constexpr (K::E1 > 0) {
+        T* dst = o1 + base * K::E1;
+        for (int idx = tid; idx < nk * K::E1; idx += NT) {
+          const int k = idx / K::E1, e = idx - k * K::E1;
+          __stcs(dst + idx, s_out[(K::E0 + e) * L + k]);
+        }
+      }
+      if constexpr (K::E2 > 0) {
+        T* dst = o2 + base * K::E2;
+        for (int idx = tid; idx < nk * K::E2; idx += NT) {
+          const int k = idx / K::E2, e = idx - k * K::E2;
+          __stcs(dst + idx, s_out[(K::E0 + K::E1 + e) * L + k]);
+        }
+      }
+      __syncthreads();
     }
   }
 }
 
 template <class K>
 constexpr size_t rbd_smem_bytes() {
-  return sizeof(typename K::T) * (size_t)K::BK * (K::SIN + (K::STAGE ? K::SOUT : 0));
+  if constexpr (K::MAP == 1)
+    return sizeof(typename K::T) * (size_t)RBD_WS_LANES *
+           (K::SIN + (K::ARENA_SMEM ? K::NA : 0) + (K::STAGE ? K::SOUT : 0));
+  else
+    return sizeof(typename K::T) * (size_t)K::BK * (K::SIN + (K::STAGE ? K::SOUT : 0));
 }
+
+// per-device cache of (CTAs per SM x SMs) and of the global arena
+struct rbd_dev_cache {
+  int grid = 0;
+  void* arena = nullptr;
+  size_t arena_bytes = 0;
+};
 
 template <class K>
 static int rbd_launch_kernel(const void* q, const void* qd, const void* u, void* o0, void* o1,
@@ -136,15 +227,42 @@ static int rbd_launch_kernel(const void* q, const void* qd, const void* u, void*
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(done & (1ull << (dev & 63)))) {
-      cudaError_t e = cudaFuncSetAttribute(rbd_batch_kernel<K>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaError_t e;
+      if constexpr (K::MAP == 1)
+        e = cudaFuncSetAttribute(rbd_ws_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      else
+        e = cudaFuncSetAttribute(rbd_batch_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
       if (e != cudaSuccess) return (int)e;
       done |= 1ull << (dev & 63);
     }
   }
-  const long long grid = (N + K::BK - 1) / K::BK;
-  rbd_batch_kernel<K><<<(unsigned)grid, K::BK, smem, (cudaStream_t)stream>>>(
-      (const T*)q, (const T*)qd, (const T*)u, (T*)o0, (T*)o1, (T*)o2, (long long)N);
+  if constexpr (K::MAP == 1) {
+    static rbd_dev_cache cache[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    rbd_dev_cache& c = cache[dev & 63];
+    if (c.grid == 0) {
+      int per_sm = 0, sms = 0;
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rbd_ws_kernel<K>, K::W * 32, smem);
+      if (e != cudaSuccess) return (int)e;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      c.grid = (per_sm > 0 ? per_sm : 1) * sms;
+      if (!K::ARENA_SMEM) {
+        c.arena_bytes = sizeof(T) * (size_t)c.grid * K::NA * 32;
+        e = cudaMalloc(&c.arena, c.arena_bytes);
+        if (e != cudaSuccess) { c.grid = 0; return (int)e; }
+      }
+    }
+    const long long groups = (N + 31) / 32;
+    const long long grid = groups < c.grid ? groups : c.grid;
+    rbd_ws_kernel<K><<<(unsigned)grid, K::W * 32, smem, (cudaStream_t)stream>>>(
+        (const T*)q, (const T*)qd, (const T*)u, (T*)o0, (T*)o1, (T*)o2, (long long)N, (T*)c.arena);
+  } else {
+    const long long grid = (N + K::BK - 1) / K::BK;
+    rbd_batch_kernel<K><<<(unsigned)grid, K::BK, smem, (cudaStream_t)stream>>>(
+        (const T*)q, (const T*)qd, (const T*)u, (T*)o0, (T*)o1, (T*)o2, (long long)N);
+  }
   return (int)cudaGetLastError();
 }
 

@@ -43,7 +43,7 @@ def _nvcc():
 
 
 def build_dir(model):
-    return os.path.join(BUILD, f"{model.name}-{codegen.model_hash(model)[:16]}")
+    return os.path.join(BUILD, f"{model.name}-{codegen.model_hash(model)[:16]}-{codegen.tuning_key()}")
 
 
 def library_path(model):
@@ -176,7 +176,7 @@ def library(model, build=True):
     """Loaded ctypes library for `model` (compiling it if needed)."""
     key = codegen.model_hash(model)
     with _LOCK:
-        lib = _LIBS.get(key)
+        lib = _LIBS.get((key, codegen.tuning_key()))
         if lib is None:
             path = library_path(model)
             if not os.path.exists(path):
@@ -187,7 +187,7 @@ def library(model, build=True):
             info = RbdInfo()
             if lib.rbd_get_info(ctypes.byref(info)) != 0 or info.fingerprint.decode() != key:
                 raise BuildError(f"library at {path} does not match model {model.name!r}")
-            _LIBS[key] = lib
+            _LIBS[(key, codegen.tuning_key())] = lib
         return lib
 
 

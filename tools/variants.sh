@@ -1,0 +1,15 @@
+#!/bin/bash
+# build (here) or time (on the GPU box) a list of tuning variants
+# usage: tools/variants.sh build|time robot alg dtype N...
+mode=$1; robot=$2; alg=$3; dt=$4; shift 4
+while read -r v; do
+  [ -z "$v" ] && continue
+  if [ "$mode" = build ]; then
+    RBD_TUNING="$v" python -c "
+import sys; sys.path.insert(0,'.')
+from paper_2109_06976_b200 import models, kernels
+kernels.compile_library(models.load('$robot'))" || echo "build failed $v"
+  else
+    RBD_TUNING="$v" timeout 300 python tools/time_kernel.py --robot $robot --alg $alg --dtype $dt --n "$@"
+  fi
+done < tools/variants.txt
