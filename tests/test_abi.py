@@ -47,5 +47,5 @@ def test_build_metadata_records_sm100a_and_registers():
     kernels.library(m)
     meta = kernels.build_meta(m)
     assert "arch=compute_100a,code=sm_100a" in " ".join(meta["nvcc_flags"])
-    assert len(meta["ptxas"]) == 10
+    assert len(meta["ptxas"]) >= 10  # thread-per-knot and/or warp-specialised kernels per (alg, dtype)
     assert all("registers" in v for v in meta["ptxas"].values())

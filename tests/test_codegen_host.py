@@ -49,7 +49,7 @@ def test_generation_is_deterministic_and_folds_constants():
     b, fb = codegen.generate_sources(m)
     assert a == b and fa == fb
     # the model's numbers are literals: no parent tables or inertia arrays in the source
-    src = a["knots_gradFD_f64.h"]
+    src = a["knots_gradFD_f64_T.h"] + a["knots_gradFD_f64_W.h"]
     assert "parent" not in src and "[6][6]" not in src
     # fewer flops than the reference program's IR count for gradFD on chain7 (17,131)
     assert fa[("gradFD", "f64")] < 17131
