@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #endif
 #include <stdint.h>
+#include <string.h>
 #include <math.h>
 
 #include "rbd_b200.h"
@@ -302,6 +303,13 @@ extern "C" int rbd_alg_extents(int alg, int32_t* n_inputs, int64_t* e0, int64_t*
 // host-buffer session: chunked H2D -> kernel -> D2H pipeline over `slots` streams
 // ---------------------------------------------------------------------------
 #define RBD_MAX_SLOTS 8
+static inline size_t rbd_align256(size_t x) { return (x + 255) & ~(size_t)255; }
+// small batches (<= RBD_ZC_BYTES of inputs + outputs) skip the copy engines:
+// the kernel reads its inputs from and writes its outputs to page-locked
+// host memory directly over PCIe (zero-copy) -- one launch + one sync.
+// Caller buffers that are already pinned are used in place; pageable ones go
+// through the session's pinned staging area with host memcpy.
+#define RBD_ZC_BYTES (4u << 20)
 struct rbd_session {
   int device;
   int64_t chunk;
@@ -309,7 +317,19 @@ struct rbd_session {
   size_t slot_bytes;
   cudaStream_t stream[RBD_MAX_SLOTS];
   unsigned char* dbuf[RBD_MAX_SLOTS];
+  unsigned char* hstage;  // pinned, RBD_ZC_BYTES
 };
+
+// device address of a host pointer when it is page-locked and mapped, else nullptr
+static inline const void* rbd_mapped(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (a.type == cudaMemoryTypeHost && a.devicePointer) return a.devicePointer;
+  return nullptr;
+}
 
 extern "C" int rbd_session_create(int device, int64_t chunk_knots, int32_t slots,
                                   rbd_session** out) {
@@ -331,6 +351,12 @@ extern "C" int rbd_session_create(int device, int64_t chunk_knots, int32_t slots
   s->chunk = chunk_knots;
   s->slots = slots;
   s->slot_bytes = (size_t)per_knot * (size_t)chunk_knots * sizeof(double) + 8 * 256;
+  e = cudaHostAlloc((void**)&s->hstage, RBD_ZC_BYTES, cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    delete s;
+    cudaSetDevice(prev);
+    return (int)e;
+  }
   for (int i = 0; i < slots; ++i) {
     e = cudaStreamCreateWithFlags(&s->stream[i], cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc((void**)&s->dbuf[i], s->slot_bytes);
@@ -339,6 +365,7 @@ extern "C" int rbd_session_create(int device, int64_t chunk_knots, int32_t slots
         if (s->dbuf[j]) cudaFree(s->dbuf[j]);
         if (s->stream[j]) cudaStreamDestroy(s->stream[j]);
       }
+      cudaFreeHost(s->hstage);
       delete s;
       cudaSetDevice(prev);
       return (int)e;
@@ -359,12 +386,11 @@ extern "C" int rbd_session_destroy(rbd_session* s) {
     cudaFree(s->dbuf[i]);
     cudaStreamDestroy(s->stream[i]);
   }
+  cudaFreeHost(s->hstage);
   cudaSetDevice(prev);
   delete s;
   return 0;
 }
-
-static inline size_t rbd_align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 extern "C" int rbd_run_host(rbd_session* s, int alg, int dtype, const void* q, const void* qd,
                             const void* u, void* out0, void* out1, void* out2, int64_t N) {
@@ -386,6 +412,46 @@ extern "C" int rbd_run_host(rbd_session* s, int alg, int dtype, const void* q, c
   cudaError_t err = cudaSetDevice(s->device);
   if (err != cudaSuccess) return (int)err;
   int rc = 0;
+  size_t in_bytes = (size_t)(e->n_inputs * N * n) * es, out_bytes = 0;
+  for (int b = 0; b < 3; ++b) out_bytes += (size_t)(N * ext[b]) * es;
+  if (in_bytes + out_bytes + 8 * 256 <= RBD_ZC_BYTES) {
+    // zero-copy: device pointers of pinned caller buffers, else the pinned stage
+    const void* din[3] = {nullptr, nullptr, nullptr};
+    void* dout[3] = {nullptr, nullptr, nullptr};
+    bool direct = true;
+    for (int a = 0; a < e->n_inputs && direct; ++a) direct = (din[a] = rbd_mapped(hin[a])) != nullptr;
+    for (int b = 0; b < 3 && direct; ++b)
+      if (ext[b]) direct = (dout[b] = (void*)rbd_mapped(hout[b])) != nullptr;
+    unsigned char* hp = s->hstage;
+    if (!direct) {
+      for (int a = 0; a < e->n_inputs; ++a) {
+        const size_t bytes = (size_t)(N * n) * es;
+        memcpy(hp, hin[a], bytes);
+        din[a] = rbd_mapped(hp);
+        hp += rbd_align256(bytes);
+      }
+      for (int b = 0; b < 3; ++b) {
+        if (!ext[b]) continue;
+        dout[b] = (void*)rbd_mapped(hp);
+        hp += rbd_align256((size_t)(N * ext[b]) * es);
+      }
+    }
+    cudaStream_t st = s->stream[0];
+    rc = e->fn(din[0], din[1], din[2], dout[0], dout[1], dout[2], N, (void*)st);
+    if (rc == 0) rc = (int)cudaStreamSynchronize(st);
+    if (rc == 0 && !direct) {
+      hp = s->hstage;
+      for (int a = 0; a < e->n_inputs; ++a) hp += rbd_align256((size_t)(N * n) * es);
+      for (int b = 0; b < 3; ++b) {
+        if (!ext[b]) continue;
+        const size_t bytes = (size_t)(N * ext[b]) * es;
+        memcpy(hout[b], hp, bytes);
+        hp += rbd_align256(bytes);
+      }
+    }
+    cudaSetDevice(prev);
+    return rc;
+  }
   for (int64_t c = 0, k0 = 0; k0 < N && rc == 0; ++c, k0 += s->chunk) {
     const int slot = (int)(c % s->slots);
     const int64_t nk = (N - k0) < s->chunk ? (N - k0) : s->chunk;

@@ -157,3 +157,30 @@ def test_full_size_properties(name, dt):
     ref = R.evaluate_batch(m, "gradFD", qs, qds, taus)
     for nm, v in (("dq_out", g.dq), ("dqd_out", g.dqd), ("qdd_out", g.qdd)):
         assert rel_err(v[idx].reshape(len(idx), -1).double().cpu().numpy(), ref[nm]) < TOL[dt]
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_path_zero_copy_and_chunked(pinned):
+    """rbd_run_host: small batches go zero-copy (pinned caller buffers in
+    place, pageable ones through the session's pinned stage); large batches
+    take the chunked H2D/kernel/D2H pipeline."""
+    from paper_2109_06976_b200 import runtime
+    for name, N in (("chain7", 100), ("quad12", 20000)):
+        m = models.load(name)
+        lib = kernels.library(m)
+        rng = np.random.default_rng(N)
+        n = m.n_dof
+        xs = [rng.uniform(-np.pi, np.pi, (N, n)), rng.uniform(-1, 1, (N, n)), rng.uniform(-1, 1, (N, n))]
+        outs = [np.full((N, e), np.nan) for _, e in codegen.outputs("gradFD", n)]
+        keep = []
+        if pinned:
+            tx = [torch.from_numpy(x).pin_memory() for x in xs]
+            to = [torch.from_numpy(o).pin_memory() for o in outs]
+            keep = tx + to
+            xs, outs = [t.numpy() for t in tx], [t.numpy() for t in to]
+        runtime.run_host(lib, "gradFD", "f64", xs, outs, N)
+        idx = rng.choice(N, size=min(N, 20), replace=False)
+        ref = R.evaluate_batch(m, "gradFD", xs[0][idx], xs[1][idx], xs[2][idx])
+        for (nm, _), o in zip(codegen.outputs("gradFD", n), outs):
+            assert rel_err(o[idx], ref[nm]) < 1e-9, (name, N, nm)
+        del keep
