@@ -705,6 +705,39 @@ def _imm(x, dtype):
     return "0f%08X" % struct.unpack(">I", struct.pack(">f", float(x)))[0]
 
 
+def _f64_needs_table(x):
+    """fp64 immediates whose low 32 bits are non-zero cannot be encoded in a
+    DFMA/DMUL instruction; ptxas would materialise them with UMOV pairs."""
+    return (struct.unpack(">Q", struct.pack(">d", float(x)))[0] & 0xFFFFFFFF) != 0
+
+
+class ConstTable:
+    """Per-kernel __constant__ table of the non-encodable fp64 immediates:
+    the PTX loads them with ld.const (ptxas turns runs of them into LDCU.128
+    uniform loads) instead of two UMOVs per use."""
+
+    def __init__(self, symbol, dtype):
+        self.symbol = symbol
+        self.on = dtype == "f64"
+        self.index = {}
+
+    def operand(self, x, lines, fresh):
+        if not self.on or not _f64_needs_table(x):
+            return _imm(x, "f64" if self.on else "f32")
+        if x not in self.index:
+            self.index[x] = len(self.index)
+        r = fresh()
+        lines.append(f"ld.const.f64 {r}, [{self.symbol}+{8 * self.index[x]}];")
+        return r
+
+    def declaration(self):
+        if not self.index:
+            return []
+        vals = sorted(self.index, key=self.index.get)
+        body = ", ".join(f"{v:.17e}" for v in vals)
+        return [f'extern "C" __constant__ double {self.symbol}[{len(vals)}] = {{{body}}};']
+
+
 def cpp_body(em, n):
     """Host C++ backend (test harness only): one statement per op."""
     lit = lambda a: _lit(a, em.dtype) if isinstance(a, float) else f"r{a}"
@@ -731,7 +764,7 @@ def cpp_body(em, n):
     return out
 
 
-def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0):
+def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None):
     """Device backend: the op list as PTX for one inline-asm block.
 
     Operand %0 is the 32-bit shared address of the knot's input row (inputs,
@@ -765,9 +798,14 @@ def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0):
     loaded = {}    # register -> index of its last load
     step = 0
 
+    def fresh():
+        nonlocal nreg
+        nreg += 1
+        return f"{R}{nreg - 1}"
+
     def use(a):
         if isinstance(a, float):
-            return imm(a)
+            return ctab.operand(a, lines, fresh) if ctab is not None else imm(a)
         if a in home and (a not in loaded or (reload_dist and step - loaded[a] > reload_dist)):
             lines.append(f"ld.shared.{t} {R}{a}, [%0+{home[a]}];")
             loaded[a] = step
@@ -862,13 +900,14 @@ def _knot_struct(model, alg, dt, name=None):
     n = L["n"]
     space = "shared" if L["stage"] else "global"
     tn = tuning(model, alg, dt)
-    body, sc = ptx_body(em, L["nin"] * n, space, tn["sync_every"], tn["reload_dist"])
+    ctab = ConstTable(f"rbd_c_{name or f'Knot_{alg}_{dt}'}", dt)
+    body, sc = ptx_body(em, L["nin"] * n, space, tn["sync_every"], tn["reload_dist"], ctab)
     src = [
         f"// GENERATED by paper_2109_06976_b200.codegen -- robot {model.name!r}, {alg} {dt}",
         f"// {em.flops} flops per knot (FMA = 2, MUL/ADD/SUB/RCP = 1); {em.nreg} SSA registers",
         "#pragma once",
         '#include "rbd_runtime.cuh"',
-    ] + _struct_head(model, alg, dt, L, em.flops, name) + [
+    ] + ctab.declaration() + _struct_head(model, alg, dt, L, em.flops, name) + [
         "  __device__ __forceinline__ static void run_dev(T* my, T* o0, T* o1, T* o2, unsigned valid) {",
     ]
     base = L["nin"] * n
@@ -935,13 +974,14 @@ def _ws_struct(model, alg, dt, warps, name=None):
     src.append("  __device__ __forceinline__ static void run_group(int warp, unsigned a_in, arena_t a_ar, "
                "out_t a0, out_t a1, out_t a2, unsigned valid) {")
     tn = tuning(model, alg, dt)
+    ctab = ConstTable(f"rbd_c_{name or f'Knot_{alg}_{dt}'}", dt)
     for p, phase in enumerate(sched.phases):
         src.append(f"    // phase {p}")
         src.append("    switch (warp) {")
         for w, tasks in enumerate(phase):
             if not tasks:
                 continue
-            body = wsched.ptx_block(sched, tasks, dt, nin * n, nin * n, ar_space, out_space, tn["reload_dist"])
+            body = wsched.ptx_block(sched, tasks, dt, nin * n, nin * n, ar_space, out_space, tn["reload_dist"], ctab)
             src.append(f"    case {w}:  // {', '.join(tasks)}")
             src.append('      asm volatile("{\\n\\t"')
             for ln in body:
@@ -953,6 +993,8 @@ def _ws_struct(model, alg, dt, warps, name=None):
         src.append("    __syncthreads();")
     src.append("    (void)a_in; (void)a_ar; (void)a0; (void)a1; (void)a2; (void)valid;")
     src += ["  }", "};", ""]
+    decl = ctab.declaration()
+    src = src[:5] + decl + src[5:]  # after the #include
     L = dict(nin=nin, ext=ext)
     return "\n".join(src), em.flops, L
 

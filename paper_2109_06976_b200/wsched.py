@@ -145,7 +145,7 @@ class Schedule:
         return sum(self.cost.values())
 
 
-def ptx_block(sched, tasks, dtype, scratch_base, nin_slots, arena_space, out_space, reload_dist=0):
+def ptx_block(sched, tasks, dtype, scratch_base, nin_slots, arena_space, out_space, reload_dist=0, ctab=None):
     """PTX for one warp's tasks in one phase.
 
     Operands: %0 = this lane's input-staging address (shared, u32),
@@ -206,8 +206,14 @@ def ptx_block(sched, tasks, dtype, scratch_base, nin_slots, arena_space, out_spa
         have[r] = step[0]
         return f"{R}{r}"
 
+    def fresh():
+        extra[0] += 1
+        return f"{R}{extra[0] - 1}"
+
     def use(a):
-        return imm(a) if isinstance(a, float) else need(a)
+        if isinstance(a, float):
+            return ctab.operand(a, lines, fresh) if ctab is not None else imm(a)
+        return need(a)
 
     def emit(op):
         k = op[0]

@@ -15,6 +15,7 @@ import numpy as np
 
 _MEM = re.compile(r"^(@%p )?(ld|st)\.(shared|global)\.(f64|f32) (.*)$")
 _ADDR = re.compile(r"\[%(\d+)\+(\d+)\]")
+_CONST = re.compile(r"^ld\.const\.f64 (\S+), \[(\w+)\+(\d+)\]$")
 
 
 def _val(tok, regs, f32):
@@ -26,7 +27,7 @@ def _val(tok, regs, f32):
     return regs[tok]
 
 
-def run_block(lines, regions, strides, valid=1, f32=False):
+def run_block(lines, regions, strides, valid=1, f32=False, consts=None):
     """lines: PTX lines (with '%%' escapes as emitted); regions[k]: dict or
     array indexed by element; strides[k]: bytes per element step of operand k."""
     rnd = (lambda x: float(np.float32(x))) if f32 else (lambda x: x)
@@ -34,6 +35,10 @@ def run_block(lines, regions, strides, valid=1, f32=False):
     for raw in lines:
         ln = raw.replace("%%", "%").strip().rstrip(";")
         if not ln or ln.startswith(".reg") or ln.startswith("setp") or ln.startswith("bar.sync"):
+            continue
+        c = _CONST.match(ln)
+        if c:
+            regs[c.group(1)] = consts[c.group(2)][int(c.group(3)) // 8]
             continue
         m = _MEM.match(ln)
         if m:

@@ -26,14 +26,16 @@ def run_thread(model, alg, dt, x, stage):
     em = codegen.generate_knot(model, alg, dt)
     n = model.n_dof
     nin = len(codegen.INPUTS[alg])
-    lines, sc = codegen.ptx_body(em, nin * n, "shared" if stage else "global")
+    ctab = codegen.ConstTable("K", dt)
+    lines, sc = codegen.ptx_body(em, nin * n, "shared" if stage else "global", ctab=ctab)
     es = 8 if dt == "f64" else 4
     row = {i: float(v) for i, v in enumerate(x)}
     for k, slot in enumerate(sc):
         row[nin * n + 2 * k] = math.sin(x[slot])
         row[nin * n + 2 * k + 1] = math.cos(x[slot])
     outs = [dict() for _ in range(3)]
-    ptxsim.run_block(lines, [row] + outs + [None], [es] * 5, f32=(dt == "f32"))
+    ptxsim.run_block(lines, [row] + outs + [None], [es] * 5, f32=(dt == "f32"),
+                     consts={"K": sorted(ctab.index, key=ctab.index.get)})
     return [np.array([o.get(i, np.nan) for i in range(e)]) for o, (_, e) in zip(outs, codegen.outputs(alg, n))]
 
 
@@ -51,12 +53,13 @@ def run_ws(model, alg, dt, x, warps, arena_space="shared", out_space="shared"):
     outs = [dict() for _ in range(3)]
     astride = L * es if arena_space == "shared" else 32 * es
     ostride = L * es if out_space == "shared" else es
+    ctab = codegen.ConstTable("K", dt)
     for phase in S.phases:
         for tasks in phase:
             if tasks:
-                lines = wsched.ptx_block(S, tasks, dt, nin * n, nin * n, arena_space, out_space)
+                lines = wsched.ptx_block(S, tasks, dt, nin * n, nin * n, arena_space, out_space, 0, ctab)
                 ptxsim.run_block(lines, [row, arena] + outs + [None], [L * es, astride, ostride, ostride, ostride],
-                                 f32=(dt == "f32"))
+                                 f32=(dt == "f32"), consts={"K": sorted(ctab.index, key=ctab.index.get)})
     return [np.array([o.get(i, np.nan) for i in range(e)]) for o, (_, e) in zip(outs, codegen.outputs(alg, n))], S
 
 
