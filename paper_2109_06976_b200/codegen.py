@@ -735,7 +735,7 @@ class ConstTable:
             return []
         vals = sorted(self.index, key=self.index.get)
         body = ", ".join(f"{v:.17e}" for v in vals)
-        return [f'extern "C" __constant__ double {self.symbol}[{len(vals)}] = {{{body}}};']
+        return [f'__constant__ double {self.symbol}[{len(vals)}] = {{{body}}};']
 
 
 def cpp_body(em, n):
