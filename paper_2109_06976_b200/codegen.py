@@ -31,6 +31,7 @@ in `csrc/rbd_runtime.cuh`; the C ABI is `include/rbd_b200.h`.
 """
 
 import hashlib
+import heapq
 import json
 import os
 import struct
@@ -205,7 +206,7 @@ class _Emit:
         return Var(acc)
 
     def vec(self, rows, hint=None):
-        return [self.lin(r) for r in rows]
+        return [self.lin(r, hint=hint) for r in rows]
 
 
 def _reg(acc):
@@ -311,7 +312,8 @@ class _Program:
         self.trees = []
         for r in model.roots():
             self.trees.append(model.subtree(r))
-        self.X = [None] * self.n
+        self.E = [None] * self.n
+        self.r = [None] * self.n
 
     # -- inputs and joint transforms -------------------------------------------
     def load_inputs(self, names):
@@ -343,22 +345,43 @@ class _Program:
                   for k in range(3)]
         else:
             raise GenerationError(f"frame {i}: fixed joints must be fused before generation")
-        sk = [[None, neg(rv[2]), rv[1]], [rv[2], None, neg(rv[0])], [neg(rv[1]), rv[0], None]]
-        Xll = [[em.lin([(-1.0, E[r][k], sk[k][c]) for k in range(3)], hint="x")
-                for c in range(3)] for r in range(3)]
-        X = [[None] * 6 for _ in range(6)]
-        for r in range(3):
-            for c in range(3):
-                X[r][c] = E[r][c]
-                X[3 + r][3 + c] = E[r][c]
-                X[3 + r][c] = Xll[r][c]
-        self.X[i] = X
+        # X_i = [[E, 0], [-E skew(r), E]] is kept factored as (E, r): the
+        # lower-left block is never materialised (xm / xtf apply it as
+        # E (l - r x w) and r x (E^T f_l)), so a joint costs registers only
+        # for the E entries that are not plain +-sin / +-cos aliases.
+        self.E[i] = E
+        self.r[i] = rv
 
     def xm(self, i, v, rows=None):
-        return mv_t(self.X[i], v, rows)
+        """rows += X_i v = [E w; E (l - r x w)]."""
+        rows = rows if rows is not None else _rows()
+        if v is None:
+            return rows
+        E, rv = self.E[i], self.r[i]
+        w, l = v[:3], v[3:]
+        rw = _rows(3)
+        _cross3(rw, 0, rv, w, -1.0)
+        t = self.em.vec([[(1.0, l[k], 1.0)] + rw[k] for k in range(3)], hint="t")
+        for r in range(3):
+            for k in range(3):
+                rows[r].append((1.0, E[r][k], w[k]))
+                rows[3 + r].append((1.0, E[r][k], t[k]))
+        return rows
 
     def xtf(self, i, f, rows=None):
-        return mtv_t(self.X[i], f, rows)
+        """rows += X_i^T f = [E^T n + r x (E^T l); E^T l]."""
+        rows = rows if rows is not None else _rows()
+        if f is None:
+            return rows
+        E, rv = self.E[i], self.r[i]
+        n_, l = f[:3], f[3:]
+        g = self.em.vec([[(1.0, E[m][k], l[m]) for m in range(3)] for k in range(3)], hint="g")
+        for k in range(3):
+            for m in range(3):
+                rows[k].append((1.0, E[m][k], n_[m]))
+            rows[3 + k].append((1.0, g[k], 1.0))
+        _cross3(rows, 0, rv, g)
+        return rows
 
     # -- RNEA (reference refdyn.py:55-88) ----------------------------------------
     def emit_rnea(self, tree, qdd, keep=False, v_in=None):
@@ -416,14 +439,13 @@ class _Program:
                 for c in range(r, 6):
                     Ia[r][c] = em.lin([(1.0, IA[i][r][c], 1.0), (-1.0, U[i][r], ud[c])], hint="ia")
                     Ia[c][r] = Ia[r][c]
-            # IA_p += X^T Ia X  (symmetric: upper triangle only)
-            X = self.X[i]
-            T_ = [[em.lin([(1.0, Ia[r][k], X[k][c]) for k in range(6)], hint="ix")
-                   for c in range(6)] for r in range(6)]
+            # IA_p += X^T Ia X  (symmetric: upper triangle only), as
+            # Y = X^T Ia column by column, then rows of Y X = (X^T Y^T)^T
+            Y = [self.em.vec(self.xtf(i, [Ia[r][c] for r in range(6)]), hint="ix") for c in range(6)]
             for r in range(6):
+                P = self.xtf(i, [Y[c][r] for c in range(6)])
                 for c in range(r, 6):
-                    IA[p][r][c] = em.lin([(1.0, IA[p][r][c], 1.0)]
-                                         + [(1.0, X[k][r], T_[k][c]) for k in range(6)], hint="ia")
+                    IA[p][r][c] = em.lin(P[c] + [(1.0, IA[p][r][c], 1.0)], hint="ia")
                     IA[p][c][r] = IA[p][r][c]
         # per column j: backward walk up the ancestors, then forward sweep
         M = {}
@@ -650,14 +672,18 @@ TUNING_DEFAULT = {
     "sync_every": 0,     # bar.sync every k PTX arithmetic ops (CTA lockstep -> shared I-cache lines)
     "reload_dist": 0,    # re-load smem-resident inputs when the last load is > k ops old (0: load once)
     "stage_kb": 64,      # stage outputs in smem when BK * outputs fit in this many KiB
+    "ra": True,          # thread: generator register allocation, spills parked in the smem row
+    "warps_per_sm": 8,   # thread + ra: target occupancy (lowered until the row fits)
+    "ra_budget": 0,      # thread + ra: cap on values kept in registers (0: from the register cap)
 }
 TUNED = {}
 for _a in ALGORITHMS:
     for _d in DTYPES:
-        # measured on B200 (profiles/variants_r1.md): the warp-specialised kernel
-        # wins at every N for the branched robots; the 30-dof thread-per-knot
-        # program spills hundreds of KB and takes ptxas minutes
-        TUNED[("quad12", _a, _d)] = {"maps": ["ws"], "warps": 16, "minb": 1}
+        # measured on B200: with outputs parked in the row, quad12's
+        # thread-per-knot kernel runs at ~80% of HBM bandwidth at N = 2^20
+        # (3.4x the warp-specialised one); humanoid30's one-knot program
+        # (~600 live values) does not fit a thread
+        TUNED[("quad12", _a, _d)] = {"warps": 16, "minb": 1}
         TUNED[("humanoid30", _a, _d)] = {"maps": ["ws"], "warps": 16, "minb": 1}
 
 
@@ -671,10 +697,20 @@ def tuning(model=None, alg=None, dtype=None):
     return t
 
 
+def _generator_sources():
+    here = os.path.dirname(os.path.abspath(__file__))
+    h = hashlib.sha256()
+    for f in ("codegen.py", "wsched.py", os.path.join("csrc", "rbd_runtime.cuh")):
+        with open(os.path.join(here, f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
 def tuning_key():
+    """Build key: generator sources + tuning knobs (a stale build is never reused)."""
     env = os.environ.get("RBD_TUNING", "")
-    return hashlib.sha256((json.dumps(TUNING_DEFAULT, sort_keys=True) + repr(sorted(TUNED.items()))
-                           + env).encode()).hexdigest()[:8]
+    return hashlib.sha256((_generator_sources() + json.dumps(TUNING_DEFAULT, sort_keys=True)
+                           + repr(sorted(TUNED.items())) + env).encode()).hexdigest()[:8]
 
 
 def knots_per_block(model, alg, dtype):
@@ -764,7 +800,137 @@ def cpp_body(em, n):
     return out
 
 
-def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None):
+def op_srcs(op):
+    """Register operands an op reads."""
+    k = op[0]
+    if k == "st":
+        args = op[3:4]
+    elif k in ("ld", "sincos"):
+        args = ()
+    else:
+        args = op[2:]
+    return [a for a in args if not isinstance(a, float)]
+
+
+def op_dsts(op):
+    k = op[0]
+    if k == "st":
+        return []
+    if k == "sincos":
+        return [op[1], op[2]]
+    return [op[1]]
+
+
+class SpillPlan:
+    """Register allocation of a straight-line op list under a budget of
+    `budget` live values, spilling to a per-thread shared-memory row.
+
+    ptxas alone spills a 200-value program to local memory, which on this
+    kernel misses L1 (the CTA's shared memory takes most of the carve-out)
+    and goes to L2.  Here the generator does it: walking the ops in order it
+    keeps at most `budget` values in registers and, when over, evicts the
+    value whose next use is furthest away (Belady), storing it once to a
+    slot of the knot's shared row; a use of an evicted value reloads it.
+    Inputs and the sin/cos scratch already live in the row (their slots are
+    their homes, and are recycled once those values die).  Slots of dead
+    values are reused, so the row is as long as the peak number of values
+    parked at once.
+
+    Result: before[i] = values to (re)load before op i, after[i] = (value,
+    slot) stores after op i, slot[v] = row slot of v, nslots = row length."""
+
+    def __init__(self, em, budget, homes, reserved, park_outputs=False, flushes=()):
+        """flushes: (op index, output k) pairs: before that op the CTA writes
+        output k back and its parked slots are recycled."""
+        ops = em.ops
+        self.park = park_outputs
+        fl = {}
+        for i, k in flushes:
+            fl.setdefault(i, []).append(k)
+        self.outslot = {}  # (output k, element) -> row slot (park_outputs)
+        self.outconst = {}  # (output k, element) -> constant value (park_outputs)
+        uses = {}
+        for i, op in enumerate(ops):
+            for a in op_srcs(op):
+                uses.setdefault(a, []).append(i)
+        ptr = dict.fromkeys(uses, 0)
+        self.slot = dict(homes)          # value -> slot (inputs, sin/cos)
+        occupied = {sl for v, sl in homes.items() if v in uses}
+        free = sorted(set(range(reserved)) - occupied)  # dead / unused input slots
+        top = reserved
+        inreg = set()
+        self.before = {}
+        self.after = {}
+        self.reloads = self.stores = 0
+        far = 1 << 40
+
+        def next_use(v):
+            p = ptr[v]
+            return uses[v][p] if p < len(uses[v]) else far
+
+        for i, op in enumerate(ops):
+            for k in fl.get(i, ()):
+                for key, sl in self.outslot.items():
+                    if key[0] == k and sl in occupied:
+                        occupied.discard(sl)
+                        heapq.heappush(free, sl)
+            srcs = op_srcs(op)
+            for a in srcs:
+                if a not in inreg:
+                    if a not in self.slot:
+                        raise GenerationError(f"value {a} used before it is defined")
+                    self.before.setdefault(i, []).append(a)
+                    self.reloads += 1
+                    inreg.add(a)
+            if park_outputs and op[0] == "st":
+                if isinstance(op[3], float):
+                    self.outconst[(op[1], op[2])] = op[3]
+                else:
+                    sl = heapq.heappop(free) if free else top
+                    if sl == top:
+                        top += 1
+                    occupied.add(sl)
+                    self.outslot[(op[1], op[2])] = sl
+            for a in srcs:
+                ptr[a] += 1
+            for a in set(srcs):
+                if ptr[a] >= len(uses[a]):
+                    inreg.discard(a)
+                    sl = self.slot.get(a)
+                    if sl is not None and sl in occupied:
+                        occupied.discard(sl)
+                        heapq.heappush(free, sl)
+            if op[0] not in ("ld", "sincos"):
+                for d in op_dsts(op):
+                    if d in uses:
+                        inreg.add(d)
+            while len(inreg) > budget:
+                v = max(inreg, key=lambda x: (next_use(x), x in self.slot))
+                inreg.discard(v)
+                if v not in self.slot:
+                    sl = heapq.heappop(free) if free else top
+                    if sl == top:
+                        top += 1
+                    occupied.add(sl)
+                    self.slot[v] = sl
+                    self.after.setdefault(i, []).append((v, sl))
+                    self.stores += 1
+        self.nslots = top
+
+
+def row_homes(em, scratch_base):
+    """Row slot of every input value and sin/cos value of the op list."""
+    homes, k = {}, 0
+    for op in em.ops:
+        if op[0] == "ld":
+            homes[op[1]] = op[2]
+        elif op[0] == "sincos":
+            homes[op[1]], homes[op[2]] = scratch_base + 2 * k, scratch_base + 2 * k + 1
+            k += 1
+    return homes
+
+
+def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None, plan=None):
     """Device backend: the op list as PTX for one inline-asm block.
 
     Operand %0 is the 32-bit shared address of the knot's input row (inputs,
@@ -775,7 +941,9 @@ def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None
     over 10^4-10^5 statements); ptxas allocates registers and schedules.
     sync_every > 0 inserts CTA barriers so all warps walk the instruction
     stream together; reload_dist > 0 re-loads smem-resident values near their
-    uses instead of keeping them live.  Returns (lines, sincos input slots).
+    uses instead of keeping them live.  With a SpillPlan the row also holds
+    the values the plan parks: loads and stores follow the plan exactly.
+    Returns (lines, sincos input slots).
     """
     t = em.dtype
     es = 8 if t == "f64" else 4
@@ -806,6 +974,8 @@ def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None
     def use(a):
         if isinstance(a, float):
             return ctab.operand(a, lines, fresh) if ctab is not None else imm(a)
+        if plan is not None:
+            return f"{R}{a}"
         if a in home and (a not in loaded or (reload_dist and step - loaded[a] > reload_dist)):
             lines.append(f"ld.shared.{t} {R}{a}, [%0+{home[a]}];")
             loaded[a] = step
@@ -813,9 +983,17 @@ def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None
 
     sc = []
     narith = 0
-    for op in em.ops:
+    for i, op in enumerate(em.ops):
         k = op[0]
         step += 1
+        if plan is not None:
+            for a in plan.before.get(i, ()):
+                lines.append(f"ld.shared.{t} {R}{a}, [%0+{plan.slot[a] * es}];")
+            if k == "sincos":
+                sc.append(op[3])
+                continue
+            if k == "ld":
+                continue
         if k == "ld":
             home[op[1]] = op[2] * es
             if not reload_dist:
@@ -850,10 +1028,17 @@ def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None
         elif k == "rcp":
             lines.append(f"rcp.rn.{t} {R}{op[1]}, {use(op[2])};")
         elif k == "st":
-            v = creg(op[3]) if isinstance(op[3], float) else use(op[3])
-            lines.append(f"{pred}st.{out_space}.{t} [%{1 + op[1]}+{op[2] * es}], {v};")
+            if plan is not None and plan.park:
+                if not isinstance(op[3], float):  # constants come from the output map
+                    lines.append(f"st.shared.{t} [%0+{plan.outslot[(op[1], op[2])] * es}], {use(op[3])};")
+            else:
+                v = creg(op[3]) if isinstance(op[3], float) else use(op[3])
+                lines.append(f"{pred}st.{out_space}.{t} [%{1 + op[1]}+{op[2] * es}], {v};")
         else:
             raise GenerationError(f"unknown op {k}")
+        if plan is not None:
+            for v, sl in plan.after.get(i, ()):
+                lines.append(f"st.shared.{t} [%0+{sl * es}], {R}{v};")
         narith += 1
         if sync_every and narith % sync_every == 0:
             lines.append("bar.sync 1;")
@@ -867,16 +1052,58 @@ def model_hash(model):
     return hashlib.sha256(model.fingerprint().encode()).hexdigest()
 
 
-def _layout(model, alg, dt, em):
+SM_SMEM = 228 * 1024      # shared memory per SM (sm_100)
+CTA_SMEM_RESERVED = 1024  # per-CTA system reservation
+REG_OVERHEAD = 16         # registers ptxas needs besides the budgeted values
+
+
+def _layout(model, alg, dt, em, device=True):
+    """Thread-per-knot launch shape and row layout.
+
+    Without the allocator ("ra": false) the row is [inputs | sin/cos] and
+    ptxas allocates registers alone.  With it, the generator keeps at most
+    B values in registers (B from the per-thread register cap at the target
+    warps per SM) and parks the rest in the knot's shared-memory row; the
+    target occupancy is lowered until the row fits the SM's shared memory."""
     n = model.n_dof
     outs = outputs(alg, n)
     ext = [e for _, e in outs] + [0] * (3 - len(outs))
     nin = len(INPUTS[alg])
     nsc = sum(1 for op in em.ops if op[0] == "sincos")
-    bk = knots_per_block(model, alg, dt)
-    stage = stage_outputs(model, alg, dt, bk)
-    return dict(n=n, ext=ext, nin=nin, nsc=nsc, bk=bk, stage=stage,
-                sin=_odd(nin * n + 2 * nsc), sout=_odd(sum(ext)))
+    tn = tuning(model, alg, dt)
+    bk = int(tn["bk"])
+    es = 8 if dt == "f64" else 4
+    base = nin * n + 2 * nsc
+    sout = _odd(sum(ext))
+    plan, minb = None, 1
+    if tn.get("ra") and device:
+        homes = row_homes(em, nin * n)
+        for warps in range(int(tn["warps_per_sm"]), 1, -1):
+            threads = 32 * warps
+            if threads % bk:
+                continue
+            ctas = threads // bk
+            regs = min(255, 65536 // threads)
+            budget = (regs - REG_OVERHEAD) // (2 if dt == "f64" else 1)
+            if tn.get("ra_budget"):
+                budget = min(budget, int(tn["ra_budget"]))
+            row_max = (SM_SMEM - ctas * (CTA_SMEM_RESERVED + 2 * sum(ext) + 16)) // (threads * es)
+            plan = SpillPlan(em, budget, homes, base, park_outputs=True)
+            if _odd(plan.nslots) <= row_max:
+                minb = ctas
+                break
+        else:
+            raise GenerationError(f"{model.name} {alg} {dt}: no occupancy fits the spill row")
+        row = _odd(max(base, plan.nslots))
+        stage = False  # outputs are parked in the row and written back coalesced
+        bad = {v for v in plan.outconst.values() if v != 0.0}
+        if bad:
+            raise GenerationError(f"{model.name} {alg}: constant outputs {bad} other than 0")
+    else:
+        row = _odd(base)
+        stage = stage_outputs(model, alg, dt, bk)
+    return dict(n=n, ext=ext, nin=nin, nsc=nsc, bk=bk, stage=stage, sin=row, sout=sout,
+                plan=plan, minb=minb, park=plan is not None)
 
 
 def _struct_head(model, alg, dt, L, fl, name=None):
@@ -888,9 +1115,28 @@ def _struct_head(model, alg, dt, L, fl, name=None):
         f"  static constexpr int E0 = {L['ext'][0]}, E1 = {L['ext'][1]}, E2 = {L['ext'][2]};",
         f"  static constexpr int SIN = {L['sin']}, SOUT = {L['sout']};",
         f"  static constexpr bool STAGE = {'true' if L['stage'] else 'false'};",
+        f"  static constexpr bool PARK = {'true' if L.get('park') else 'false'};  // outputs parked in the row",
         f"  static constexpr int FLOPS = {fl};",
         "  static constexpr int MAP = 0;  // thread per knot",
+        f"  static constexpr int MINB = {L.get('minb', 1)};  // CTAs per SM the row layout is sized for",
     ]
+
+
+def _omap_decl(L, name):
+    """Parked-output map: output element e (outputs concatenated in
+    output_map order) -> row slot holding it, or -1 for a structural 0."""
+    if not L.get("park"):
+        return []
+    plan = L["plan"]
+    vals = []
+    for k, e in enumerate(L["ext"]):
+        for idx in range(e):
+            vals.append(plan.outslot.get((k, idx), -1))
+    for k, e in enumerate(L["ext"]):
+        for idx in range(e):
+            if (k, idx) not in plan.outslot and (k, idx) not in plan.outconst:
+                raise GenerationError(f"output {k}[{idx}] is never written")
+    return [f"__constant__ short rbd_om_{name}[{len(vals)}] = {{{', '.join(map(str, vals))}}};"]
 
 
 def _knot_struct(model, alg, dt, name=None):
@@ -901,15 +1147,22 @@ def _knot_struct(model, alg, dt, name=None):
     space = "shared" if L["stage"] else "global"
     tn = tuning(model, alg, dt)
     ctab = ConstTable(f"rbd_c_{name or f'Knot_{alg}_{dt}'}", dt)
-    body, sc = ptx_body(em, L["nin"] * n, space, tn["sync_every"], tn["reload_dist"], ctab)
+    plan = L["plan"]
+    body, sc = ptx_body(em, L["nin"] * n, space, tn["sync_every"], tn["reload_dist"], ctab, plan)
+    ra = (f"// register budget: {plan.reloads} reloads, {plan.stores} parked values, row {L['sin']} slots, "
+          f"{L['minb']} CTAs of {L['bk']} per SM" if plan is not None else "// ptxas register allocation")
     src = [
         f"// GENERATED by paper_2109_06976_b200.codegen -- robot {model.name!r}, {alg} {dt}",
         f"// {em.flops} flops per knot (FMA = 2, MUL/ADD/SUB/RCP = 1); {em.nreg} SSA registers",
+        ra,
         "#pragma once",
         '#include "rbd_runtime.cuh"',
-    ] + ctab.declaration() + _struct_head(model, alg, dt, L, em.flops, name) + [
+    ] + ctab.declaration() + _omap_decl(L, name or f"Knot_{alg}_{dt}") \
+        + _struct_head(model, alg, dt, L, em.flops, name) + [
         "  __device__ __forceinline__ static void run_dev(T* my, T* o0, T* o1, T* o2, unsigned valid) {",
     ]
+    if L.get("park"):
+        src.insert(-1, f"  __device__ __forceinline__ static const short* omap() {{ return rbd_om_{name or f'Knot_{alg}_{dt}'}; }}")
     base = L["nin"] * n
     for k, slot in enumerate(sc):
         src.append(f"    {{ T s, c; rbd_sincos(my[{slot}], &s, &c); my[{base + 2 * k}] = s; my[{base + 2 * k + 1}] = c; }}")
@@ -1010,7 +1263,7 @@ def host_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
     for alg in algorithms:
         for dt in dtypes:
             em = generate_knot(model, alg, dt)
-            L = _layout(model, alg, dt, em)
+            L = _layout(model, alg, dt, em, device=False)
             src = ["#pragma once", '#include "rbd_runtime.cuh"'] + _struct_head(model, alg, dt, L, em.flops) + [
                 "  static inline void run(const T* __restrict__ iq, const T* __restrict__ iqd,",
                 "                         const T* __restrict__ iu, T* __restrict__ o0,",

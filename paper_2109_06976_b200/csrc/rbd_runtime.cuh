@@ -56,7 +56,7 @@ RBD_HD float rbd_fma(float a, float b, float c) { return fmaf(a, b, c); }
 // batch kernel: CTA = BK knots, thread t = knot (blockIdx.x * BK + t)
 // ---------------------------------------------------------------------------
 template <class K>
-__global__ void __launch_bounds__(K::BK)
+__global__ void __launch_bounds__(K::BK, K::MINB)
 rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __restrict__ qd,
                  const typename K::T* __restrict__ u, typename K::T* __restrict__ o0,
                  typename K::T* __restrict__ o1, typename K::T* __restrict__ o2, long long N) {
@@ -70,19 +70,53 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
   const int nk = left < BK ? (int)left : BK;
   const int tid = threadIdx.x;
 
+  // all NIN * n loads of this thread are issued before the first smem store
+  // (one HBM round trip per CTA, not one per element)
+  T v[K::NIN][n];
 #pragma unroll
   for (int a = 0; a < K::NIN; ++a) {
     const T* src = (a == 0 ? q : (a == 1 ? qd : u)) + base * n;
-    T* dst = s_in + a * n;
-    for (int idx = tid; idx < BK * n; idx += BK) {
-      const int k = idx / n, j = idx - k * n;
-      dst[k * K::SIN + j] = (k < nk) ? __ldg(src + idx) : T(0);
+#pragma unroll
+    for (int r = 0; r < n; ++r) {
+      const int idx = tid + r * BK;
+      v[a][r] = (idx < nk * n) ? __ldg(src + idx) : T(0);
     }
+  }
+#pragma unroll
+  for (int a = 0; a < K::NIN; ++a) {
+#pragma unroll
+    for (int r = 0; r < n; ++r) {
+      const int idx = tid + r * BK;
+      const int k = idx / n, j = idx - k * n;
+      s_in[k * K::SIN + a * n + j] = v[a][r];
+    }
+  }
+  constexpr int EALL = K::E0 + K::E1 + K::E2;
+  short* s_map = reinterpret_cast<short*>(s_in + BK * K::SIN);  // PARK: output element -> row slot
+  if constexpr (K::PARK) {
+    for (int e = tid; e < EALL; e += BK) s_map[e] = K::omap()[e];
   }
   __syncthreads();
   T* my = s_in + tid * K::SIN;  // this knot's inputs + its sin/cos scratch
 
-  if constexpr (K::STAGE) {
+  if constexpr (K::PARK) {
+    // the program parks every output value in its row; write the CTA's
+    // contiguous output ranges back coalesced (structural zeros from the map)
+    K::run_dev(my, nullptr, nullptr, nullptr, 1u);
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      const int E = b == 0 ? K::E0 : (b == 1 ? K::E1 : K::E2);
+      const int off = b == 0 ? 0 : (b == 1 ? K::E0 : K::E0 + K::E1);
+      if (E == 0) continue;
+      T* dst = (b == 0 ? o0 : (b == 1 ? o1 : o2)) + base * E;
+      for (int idx = tid; idx < nk * E; idx += BK) {
+        const int k = idx / E, e = idx - k * E;
+        const int sl = s_map[off + e];
+        __stcs(dst + idx, sl >= 0 ? s_in[k * K::SIN + sl] : T(0));
+      }
+    }
+  } else if constexpr (K::STAGE) {
     T* o = s_out + tid * K::SOUT;
     K::run_dev(my, o, o + K::E0, o + K::E0 + K::E1, 1u);
     __syncthreads();
@@ -141,12 +175,26 @@ rbd_ws_kernel(const typename K::T* __restrict__ q, const typename K::T* __restri
   for (long long g = blockIdx.x; g < groups; g += gridDim.x) {
     const long long base = g * 32;
     const int nk = (N - base) < 32 ? (int)(N - base) : 32;
+    constexpr int PER = (32 * n + NT - 1) / NT;  // loads per thread per input
+    T v[K::NIN][PER];
 #pragma unroll
     for (int a = 0; a < K::NIN; ++a) {
       const T* src = (a == 0 ? q : (a == 1 ? qd : u)) + base * n;
-      for (int idx = tid; idx < 32 * n; idx += NT) {
-        const int k = idx / n, j = idx - k * n;
-        s_in[(a * n + j) * L + k] = (k < nk) ? __ldg(src + idx) : T(0);
+#pragma unroll
+      for (int r = 0; r < PER; ++r) {
+        const int idx = tid + r * NT;
+        v[a][r] = (idx < nk * n) ? __ldg(src + idx) : T(0);
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < K::NIN; ++a) {
+#pragma unroll
+      for (int r = 0; r < PER; ++r) {
+        const int idx = tid + r * NT;
+        if (idx < 32 * n) {
+          const int k = idx / n, j = idx - k * n;
+          s_in[(a * n + j) * L + k] = v[a][r];
+        }
       }
     }
     __syncthreads();
@@ -203,7 +251,8 @@ constexpr size_t rbd_smem_bytes() {
     return sizeof(typename K::T) * (size_t)RBD_WS_LANES *
            (K::SIN + (K::ARENA_SMEM ? K::NA : 0) + (K::STAGE ? K::SOUT : 0));
   else
-    return sizeof(typename K::T) * (size_t)K::BK * (K::SIN + (K::STAGE ? K::SOUT : 0));
+    return sizeof(typename K::T) * (size_t)K::BK * (K::SIN + (K::STAGE ? K::SOUT : 0)) +
+           (K::PARK ? sizeof(short) * (size_t)(K::E0 + K::E1 + K::E2) : 0);
 }
 
 // per-device cache of (CTAs per SM x SMs) and of the global arena

@@ -17,7 +17,7 @@ OUT = os.path.join(os.path.dirname(HERE), "_hostbuild")
 
 
 def host_library(model, opt="-O0"):
-    d = os.path.join(OUT, f"{model.name}-{codegen.model_hash(model)[:16]}")
+    d = os.path.join(OUT, f"{model.name}-{codegen.model_hash(model)[:16]}-{codegen.tuning_key()}")
     so = os.path.join(d, "host.so")
     if not os.path.exists(so):
         os.makedirs(d, exist_ok=True)

@@ -52,6 +52,33 @@ def test_all_algorithms_match_reference(name, dt):
             assert rel_err(v, refs[nm]) < TOL[dt], (name, alg, dt, nm, rel_err(v, refs[nm]))
 
 
+@pytest.mark.parametrize("name", MODELS)
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_large_batch_mapping_matches_reference(name, dt):
+    """Above the small-batch threshold the library launches the other kernel
+    mapping (thread per knot with its register plan and parked outputs):
+    golden knots tiled to N = threshold + 37 (ragged last CTA), every knot
+    checked."""
+    g = golden(name)
+    m = models.load(name)
+    N = int(codegen.tuning(m, "gradFD", dt)["ws_max_n"]) + 37
+    reps = -(-N // g["q"].shape[0])
+    tile = lambda x: np.tile(x, (reps, 1))[:N]
+    for alg in codegen.ALGORITHMS:
+        if dt == "f64":
+            q, qd, u = (tile(g[k]) for k in ("q", "qd", "u"))
+            refs = {nm: tile(g[f"{alg}.{nm}"]) for nm, _ in codegen.outputs(alg, m.n_dof)}
+        else:
+            q32, qd32, u32 = (g[k].astype(np.float32) for k in ("q", "qd", "u"))
+            r = R.evaluate_batch(m, alg, q32.astype(np.float64), qd32.astype(np.float64), u32.astype(np.float64))
+            q, qd, u = tile(q32), tile(qd32), tile(u32)
+            refs = {nm: tile(v) for nm, v in r.items()}
+        out = _device_eval(m, alg, dt, q, qd, u)
+        for nm, v in out.items():
+            assert np.all(np.isfinite(v)), (name, alg, nm)
+            assert rel_err(v, refs[nm]) < TOL[dt], (name, alg, dt, nm, rel_err(v, refs[nm]))
+
+
 @pytest.mark.parametrize("name", ["quad12", "humanoid30"])
 def test_cross_tree_blocks_exact_zero(name):
     g = golden(name)

@@ -22,12 +22,17 @@ def _sincos_slots(em):
     return [op[3] for op in em.ops if op[0] == "sincos"]
 
 
-def run_thread(model, alg, dt, x, stage):
+def run_thread(model, alg, dt, x, stage, budget=None, park=False):
     em = codegen.generate_knot(model, alg, dt)
     n = model.n_dof
     nin = len(codegen.INPUTS[alg])
     ctab = codegen.ConstTable("K", dt)
-    lines, sc = codegen.ptx_body(em, nin * n, "shared" if stage else "global", ctab=ctab)
+    plan = None
+    if budget:
+        nsc = len(_sincos_slots(em))
+        plan = codegen.SpillPlan(em, budget, codegen.row_homes(em, nin * n), nin * n + 2 * nsc,
+                                 park_outputs=park)
+    lines, sc = codegen.ptx_body(em, nin * n, "shared" if stage else "global", ctab=ctab, plan=plan)
     es = 8 if dt == "f64" else 4
     row = {i: float(v) for i, v in enumerate(x)}
     for k, slot in enumerate(sc):
@@ -36,6 +41,11 @@ def run_thread(model, alg, dt, x, stage):
     outs = [dict() for _ in range(3)]
     ptxsim.run_block(lines, [row] + outs + [None], [es] * 5, f32=(dt == "f32"),
                      consts={"K": sorted(ctab.index, key=ctab.index.get)})
+    if park:  # the kernel's write-back: parked row slots, structural zeros
+        for (k, idx), sl in plan.outslot.items():
+            outs[k][idx] = row[sl]
+        for (k, idx), v in plan.outconst.items():
+            outs[k][idx] = v
     return [np.array([o.get(i, np.nan) for i in range(e)]) for o, (_, e) in zip(outs, codegen.outputs(alg, n))]
 
 
@@ -64,7 +74,7 @@ def run_ws(model, alg, dt, x, warps, arena_space="shared", out_space="shared"):
 
 
 @pytest.mark.parametrize("name", ["pendulum2", "chain7", "tree7", "mixed5", "quad12"])
-@pytest.mark.parametrize("mapping", ["thread", "ws"])
+@pytest.mark.parametrize("mapping", ["thread", "thread_ra", "thread_park", "ws"])
 def test_device_ptx_matches_reference(name, mapping):
     g = golden(name)
     m = models.load(name)
@@ -74,6 +84,12 @@ def test_device_ptx_matches_reference(name, mapping):
             x = _inputs(g, alg, k, n)
             if mapping == "thread":
                 outs = run_thread(m, alg, "f64", x, stage=(k == 0))
+            elif mapping == "thread_park":
+                # the product layout: outputs parked in the row, written back by map
+                outs = run_thread(m, alg, "f64", x, stage=False, budget=16 if k == 0 else 119, park=True)
+            elif mapping == "thread_ra":
+                # tight register budgets force heavy parking / slot reuse
+                outs = run_thread(m, alg, "f64", x, stage=(k == 0), budget=12 if k == 0 else 40)
             else:
                 outs, _ = run_ws(m, alg, "f64", x, warps=4 if k == 0 else 7,
                                  arena_space="shared" if k == 0 else "global",

@@ -1,8 +1,7 @@
 #!/bin/bash
-# one gpurun call: GPU tests, smoke, a quick bench, launch list
+# one gpurun call: GPU tests, smoke, a quick bench
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 600 python bench.py --steps 10 --warmup 3 --no-sweep > gpurun_out/bench_quick.json 2> gpurun_out/bench_quick.err; echo "bench rc=$?" >> gpurun_out/bench_quick.err
-tail -5 gpurun_out/pytest_gpu.log; cat gpurun_out/smoke.log; cat gpurun_out/bench_quick.json; tail -5 gpurun_out/bench_quick.err
+timeout 600 python bench.py --steps 10 --warmup 3 --no-sweep --no-cpu > gpurun_out/bench_quick.json 2> gpurun_out/bench_quick.err; echo "bench rc=$?" >> gpurun_out/bench_quick.err
+tail -3 gpurun_out/pytest_gpu.log; cat gpurun_out/smoke.log; cut -c1-600 gpurun_out/bench_quick.json; tail -3 gpurun_out/bench_quick.err

@@ -12,4 +12,4 @@ kernels.compile_library(models.load('$robot'))" || echo "build failed $v"
   else
     RBD_TUNING="$v" timeout 300 python tools/time_kernel.py --robot $robot --alg $alg --dtype $dt --n "$@"
   fi
-done < tools/variants.txt
+done < ${VARIANTS:-tools/variants.txt}
