@@ -114,6 +114,7 @@ class _Emit:
         self.task = "main"
         self.nreg = 0
         self.flops = 0  # FMA = 2, MUL/ADD/SUB/RCP = 1 (the reference's counting rule)
+        self.lo, self.np = 0, 0  # input dof window of the program (set by _Program.run)
 
     def reg(self):
         self.nreg += 1
@@ -317,11 +318,13 @@ class _Program:
 
     # -- inputs and joint transforms -------------------------------------------
     def load_inputs(self, names):
-        """Per-knot input row: q at slots [0, n), qd at [n, 2n), u at [2n, 3n)."""
+        """Per-knot input row: the program's dof window [lo, lo + np) of each
+        input, q at slots [0, np), qd at [np, 2np), u at [2np, 3np)."""
         em = self.em
+        lo, np_ = em.lo, em.np
         self.inp = {}
         for a, nm in enumerate(names):
-            self.inp[nm] = [em.load(a * self.n + i) for i in range(self.n)]
+            self.inp[nm] = [em.load(a * np_ + i - lo) if lo <= i < lo + np_ else None for i in range(self.n)]
 
     def emit_xform(self, i):
         """X_i = [[E, 0], [-E skew(r), E]] as an entry grid (folded)."""
@@ -334,7 +337,7 @@ class _Program:
             A = (np.eye(3) + K @ K) @ E0
             B = K @ E0
             C = K @ K @ E0
-            sv, cv = em.sincos(i)  # q_i sits in input slot i
+            sv, cv = em.sincos(i - em.lo)  # q_i sits in input slot i - lo
             E = [[em.lin([(-float(B[r, k]), sv, 1.0), (-float(C[r, k]), cv, 1.0)],
                          c0=float(A[r, k]), hint="e") for k in range(3)] for r in range(3)]
             rv = _const_vec(j.origin_translation)
@@ -559,20 +562,28 @@ class _Program:
     def store(self, slot, idx, e):
         self.em.store(int(slot[1]), idx, e)
 
-    def run(self):
+    def run(self, trees=None, zero_fill=True, cols=None):
         """Emit the whole one-knot program.  Every op carries a task tag:
         'in' / 'xf' (input loads, joint transforms: re-materialised by each
         consumer), then per root tree t: rnea0.t, ia.t, minv.t.j, fd.t,
         rnea1.t, grad.t.<q|qd>.c, zeros.  The thread-per-knot mapping ignores
         the tags; the warp-specialised mapping schedules tasks over warps."""
         alg, n, em = self.alg, self.n, self.em
+        part = [t for t in range(len(self.trees)) if trees is None or t in trees]
+        dofs = sorted(i for t in part for i in self.trees[t])
+        if not dofs or dofs != list(range(dofs[0], dofs[-1] + 1)):
+            raise GenerationError(f"part {trees}: its trees must cover a contiguous dof range")
+        em.lo, em.np = dofs[0], len(dofs)
         em.task = "in"
         self.load_inputs(INPUTS[alg])
         em.task = "xf"
         for i in range(n):
-            self.emit_xform(i)
+            if any(i in self.trees[t] for t in part):
+                self.emit_xform(i)
         stored = set()
         for t, tree in enumerate(self.trees):
+            if t not in part:
+                continue
             if alg == "ID":
                 em.task = f"rnea0.{t}"
                 R = self.emit_rnea(tree, self.inp["qdd"])
@@ -593,6 +604,8 @@ class _Program:
                 self.emit_xcf(tree, R)
                 for o, kind in (("o0", "q"), ("o1", "qd")):
                     for c in tree:
+                        if cols is not None and c not in cols:
+                            continue
                         em.task = f"grad.{t}.{kind}.{c}"
                         dc = self.emit_grad_column(tree, kind, c, R)
                         for i in tree:
@@ -600,13 +613,16 @@ class _Program:
                             stored.add(i * n + c)
             elif alg == "gradFD":
                 qdd, M, R0 = self._fd(tree, t)
-                for i in tree:
-                    self.store("o2", i, qdd[i])
+                if cols is None or tree[0] in cols:
+                    for i in tree:
+                        self.store("o2", i, qdd[i])
                 em.task = f"rnea1.{t}"
                 R = self.emit_rnea(tree, qdd, v_in=(R0["v"], R0["Xv"]))
                 self.emit_xcf(tree, R)
                 for o, kind in (("o0", "q"), ("o1", "qd")):
                     for c in tree:
+                        if cols is not None and c not in cols:
+                            continue
                         em.task = f"grad.{t}.{kind}.{c}"
                         dc = self.emit_grad_column(tree, kind, c, R)
                         for i in tree:
@@ -615,7 +631,7 @@ class _Program:
                             stored.add(i * n + c)
             else:
                 raise GenerationError(f"unsupported algorithm {alg!r}")
-        if alg in ("Minv", "gradID", "gradFD"):
+        if alg in ("Minv", "gradID", "gradFD") and zero_fill:
             # cross-tree blocks are structurally zero
             em.task = "zeros"
             for o in (("o0",) if alg == "Minv" else ("o0", "o1")):
@@ -684,7 +700,10 @@ for _a in ALGORITHMS:
         # (3.4x the warp-specialised one); humanoid30's one-knot program
         # (~600 live values) does not fit a thread
         TUNED[("quad12", _a, _d)] = {"warps": 16, "minb": 1}
-        TUNED[("humanoid30", _a, _d)] = {"maps": ["ws"], "warps": 16, "minb": 1}
+        # humanoid30: small batches on the warp-specialised kernel; large ones
+        # per root tree (torso tree, two legs)
+        TUNED[("humanoid30", _a, _d)] = {"maps": ["ws"], "warps": 16, "minb": 1, "parts": [[0], [1], [2]],
+                                         "zero_memset": True}
 
 
 def tuning(model=None, alg=None, dtype=None):
@@ -725,9 +744,11 @@ def stage_outputs(model, alg, dtype, bk):
     return bk * _odd(ext) * es <= tuning(model, alg, dtype)["stage_kb"] * 1024
 
 
-def generate_knot(model, alg, dtype):
-    """The one-knot program as an op list (`_Emit`)."""
-    return _Program(model, alg, dtype).run()
+def generate_knot(model, alg, dtype, trees=None, zero_fill=True, cols=None):
+    """The one-knot program as an op list (`_Emit`).  trees: restrict to
+    these root trees (a 'part'; its outputs are the trees' blocks);
+    zero_fill: also store the structural zeros outside the blocks emitted."""
+    return _Program(model, alg, dtype).run(trees, zero_fill, None if cols is None else frozenset(cols))
 
 
 def _lit(x, dtype):
@@ -781,9 +802,9 @@ def cpp_body(em, n):
     for op in em.ops:
         k = op[0]
         if k == "ld":
-            out.append(f"const T r{op[1]} = {('iq', 'iqd', 'iu')[op[2] // n]}[{op[2] % n}];")
+            out.append(f"const T r{op[1]} = {('iq', 'iqd', 'iu')[op[2] // em.np]}[{em.lo + op[2] % em.np}];")
         elif k == "sincos":
-            out.append(f"T r{op[1]}, r{op[2]}; rbd_sincos(iq[{op[3]}], &r{op[1]}, &r{op[2]});")
+            out.append(f"T r{op[1]}, r{op[2]}; rbd_sincos(iq[{em.lo + op[3]}], &r{op[1]}, &r{op[2]});")
         elif k == "fma":
             out.append(f"const T r{op[1]} = rbd_fma({lit(op[2])}, {lit(op[3])}, {lit(op[4])});")
         elif k in ("mul", "add", "sub"):
@@ -1073,11 +1094,11 @@ def _layout(model, alg, dt, em, device=True):
     tn = tuning(model, alg, dt)
     bk = int(tn["bk"])
     es = 8 if dt == "f64" else 4
-    base = nin * n + 2 * nsc
+    base = nin * em.np + 2 * nsc
     sout = _odd(sum(ext))
     plan, minb = None, 1
     if tn.get("ra") and device:
-        homes = row_homes(em, nin * n)
+        homes = row_homes(em, nin * em.np)
         for warps in range(int(tn["warps_per_sm"]), 1, -1):
             threads = 32 * warps
             if threads % bk:
@@ -1087,7 +1108,7 @@ def _layout(model, alg, dt, em, device=True):
             budget = (regs - REG_OVERHEAD) // (2 if dt == "f64" else 1)
             if tn.get("ra_budget"):
                 budget = min(budget, int(tn["ra_budget"]))
-            row_max = (SM_SMEM - ctas * (CTA_SMEM_RESERVED + 2 * sum(ext) + 16)) // (threads * es)
+            row_max = (SM_SMEM - ctas * (CTA_SMEM_RESERVED + 4 * sum(ext) + 16)) // (threads * es)
             plan = SpillPlan(em, budget, homes, base, park_outputs=True)
             if _odd(plan.nslots) <= row_max:
                 minb = ctas
@@ -1103,7 +1124,7 @@ def _layout(model, alg, dt, em, device=True):
         row = _odd(base)
         stage = stage_outputs(model, alg, dt, bk)
     return dict(n=n, ext=ext, nin=nin, nsc=nsc, bk=bk, stage=stage, sin=row, sout=sout,
-                plan=plan, minb=minb, park=plan is not None)
+                plan=plan, minb=minb, park=plan is not None, lo=em.lo, np=em.np)
 
 
 def _struct_head(model, alg, dt, L, fl, name=None):
@@ -1112,6 +1133,7 @@ def _struct_head(model, alg, dt, L, fl, name=None):
         f"struct {name or f'Knot_{alg}_{dt}'} {{",
         f"  typedef {T} T;",
         f"  static constexpr int NDOF = {L['n']}, NIN = {L['nin']}, BK = {L['bk']};",
+        f"  static constexpr int LO = {L['lo']}, NP = {L['np']};  // input dof window [LO, LO + NP)",
         f"  static constexpr int E0 = {L['ext'][0]}, E1 = {L['ext'][1]}, E2 = {L['ext'][2]};",
         f"  static constexpr int SIN = {L['sin']}, SOUT = {L['sout']};",
         f"  static constexpr bool STAGE = {'true' if L['stage'] else 'false'};",
@@ -1122,33 +1144,50 @@ def _struct_head(model, alg, dt, L, fl, name=None):
     ]
 
 
+def _omap(L):
+    """Parked-output list of the program: [(element, slot)] in element order,
+    element = index into the outputs concatenated in output_map order, slot
+    = row slot holding it or -1 for a structural 0.  A part program (a subset
+    of the root trees) lists only the elements it writes."""
+    plan = L["plan"]
+    out, base = [], 0
+    for k, e in enumerate(L["ext"]):
+        for idx in range(e):
+            if (k, idx) in plan.outslot:
+                out.append((base + idx, plan.outslot[(k, idx)]))
+            elif (k, idx) in plan.outconst:
+                out.append((base + idx, -1))
+        base += e
+    return out
+
+
 def _omap_decl(L, name):
-    """Parked-output map: output element e (outputs concatenated in
-    output_map order) -> row slot holding it, or -1 for a structural 0."""
     if not L.get("park"):
         return []
-    plan = L["plan"]
-    vals = []
-    for k, e in enumerate(L["ext"]):
-        for idx in range(e):
-            vals.append(plan.outslot.get((k, idx), -1))
-    for k, e in enumerate(L["ext"]):
-        for idx in range(e):
-            if (k, idx) not in plan.outslot and (k, idx) not in plan.outconst:
-                raise GenerationError(f"output {k}[{idx}] is never written")
-    return [f"__constant__ short rbd_om_{name}[{len(vals)}] = {{{', '.join(map(str, vals))}}};"]
+    om = _omap(L)
+    full = [e for e, _ in om] == list(range(sum(L["ext"])))
+    if full is False and L.get("full_outputs"):
+        raise GenerationError(f"{name}: some outputs are never written")
+    if sum(L["ext"]) > 65535:
+        raise GenerationError(f"{name}: output map too large")
+    L["nout"], L["ofull"] = len(om), full
+    lines = [f"__constant__ short rbd_om_{name}[{len(om)}] = {{{', '.join(str(sl) for _, sl in om)}}};"]
+    if not full:
+        lines.append(f"__constant__ unsigned short rbd_oe_{name}[{len(om)}] = "
+                     f"{{{', '.join(str(e) for e, _ in om)}}};")
+    return lines
 
 
-def _knot_struct(model, alg, dt, name=None):
+def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True):
     """Device header: C++ sin/cos prologue + the PTX body in one asm block."""
-    em = generate_knot(model, alg, dt)
+    em = generate_knot(model, alg, dt, trees, zero_fill)
     L = _layout(model, alg, dt, em)
     n = L["n"]
     space = "shared" if L["stage"] else "global"
     tn = tuning(model, alg, dt)
     ctab = ConstTable(f"rbd_c_{name or f'Knot_{alg}_{dt}'}", dt)
     plan = L["plan"]
-    body, sc = ptx_body(em, L["nin"] * n, space, tn["sync_every"], tn["reload_dist"], ctab, plan)
+    body, sc = ptx_body(em, L["nin"] * em.np, space, tn["sync_every"], tn["reload_dist"], ctab, plan)
     ra = (f"// register budget: {plan.reloads} reloads, {plan.stores} parked values, row {L['sin']} slots, "
           f"{L['minb']} CTAs of {L['bk']} per SM" if plan is not None else "// ptxas register allocation")
     src = [
@@ -1162,8 +1201,13 @@ def _knot_struct(model, alg, dt, name=None):
         "  __device__ __forceinline__ static void run_dev(T* my, T* o0, T* o1, T* o2, unsigned valid) {",
     ]
     if L.get("park"):
-        src.insert(-1, f"  __device__ __forceinline__ static const short* omap() {{ return rbd_om_{name or f'Knot_{alg}_{dt}'}; }}")
-    base = L["nin"] * n
+        nm = name or f"Knot_{alg}_{dt}"
+        src.insert(-1, f"  static constexpr int NOUT = {L['nout']};  // output elements this program writes")
+        src.insert(-1, f"  static constexpr bool OFULL = {'true' if L['ofull'] else 'false'};  // ... all of them, in order")
+        src.insert(-1, f"  __device__ __forceinline__ static const short* omap() {{ return rbd_om_{nm}; }}")
+        src.insert(-1, "  __device__ __forceinline__ static const unsigned short* oelem() { return "
+                   + (f"rbd_oe_{nm}" if not L["ofull"] else "nullptr") + "; }")
+    base = L["nin"] * em.np
     for k, slot in enumerate(sc):
         src.append(f"    {{ T s, c; rbd_sincos(my[{slot}], &s, &c); my[{base + 2 * k}] = s; my[{base + 2 * k + 1}] = c; }}")
     src.append("    const unsigned a_in = (unsigned)__cvta_generic_to_shared(my);")
@@ -1181,10 +1225,10 @@ def _knot_struct(model, alg, dt, name=None):
     return "\n".join(src), em.flops, L
 
 
-def _ws_struct(model, alg, dt, warps, name=None):
+def _ws_struct(model, alg, dt, warps, name=None, trees=None, zero_fill=True):
     """Device header of the warp-specialised mapping (see wsched.py)."""
     from . import wsched
-    P = wsched.plan(model, alg, dt, warps)
+    P = wsched.plan(model, alg, dt, warps, trees, zero_fill)
     em, sched = P["em"], P["sched"]
     n, nin = P["n"], P["nin"]
     T = "double" if dt == "f64" else "float"
@@ -1205,6 +1249,7 @@ def _ws_struct(model, alg, dt, warps, name=None):
         f"  typedef {T} T;",
         "  static constexpr int MAP = 1;  // warp-specialised: CTA = 32 knots x W warps",
         f"  static constexpr int W = {warps}, NDOF = {n}, NIN = {nin}, NSC = {P['nsc']};",
+        f"  static constexpr int LO = {em.lo}, NP = {em.np};  // input dof window [LO, LO + NP)",
         f"  static constexpr int E0 = {ext[0]}, E1 = {ext[1]}, E2 = {ext[2]};",
         f"  static constexpr int SIN = {P['sin']}, NA = {sched.nslots}, SOUT = {P['sout']};",
         f"  static constexpr bool STAGE = {'true' if P['stage'] else 'false'}, "
@@ -1220,7 +1265,7 @@ def _ws_struct(model, alg, dt, warps, name=None):
         if op[0] == "sincos":
             slot = op[3]
             src.append(f"    if (warp == {k % warps}) {{ T s, c; rbd_sincos(s_in[{slot * 33} + lane], &s, &c); "
-                       f"s_in[{(nin * n + 2 * k) * 33} + lane] = s; s_in[{(nin * n + 2 * k + 1) * 33} + lane] = c; }}")
+                       f"s_in[{(nin * em.np + 2 * k) * 33} + lane] = s; s_in[{(nin * em.np + 2 * k + 1) * 33} + lane] = c; }}")
             k += 1
     src.append("    (void)s_in; (void)warp; (void)lane;")
     src.append("  }")
@@ -1234,7 +1279,8 @@ def _ws_struct(model, alg, dt, warps, name=None):
         for w, tasks in enumerate(phase):
             if not tasks:
                 continue
-            body = wsched.ptx_block(sched, tasks, dt, nin * n, nin * n, ar_space, out_space, tn["reload_dist"], ctab)
+            body = wsched.ptx_block(sched, tasks, dt, nin * em.np, nin * em.np, ar_space, out_space,
+                                    tn["reload_dist"], ctab)
             src.append(f"    case {w}:  // {', '.join(tasks)}")
             src.append('      asm volatile("{\\n\\t"')
             for ln in body:
@@ -1310,14 +1356,56 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
                     "}",
                     "",
                 ])
+            # large batches of a robot with several root trees: one kernel per
+            # part (a group of trees), each mapped on its own (thread per knot
+            # when its register plan fits, else warp-specialised); the first
+            # part also writes the cross-part structural zeros
+            parts = tn.get("parts") or []
+            # cross-part structural zeros: a coalesced memset of the n x n
+            # outputs before the parts ("memset"), or stores in part 0
+            zf = not tn.get("zero_memset")
+            ptags = []
+            for pi, trees in enumerate(parts):
+                tag = f"P{pi}"
+                K = f"Knot_{alg}_{dt}_{tag}"
+                try:
+                    text, fl, L = _knot_struct(model, alg, dt, K, trees=tuple(trees), zero_fill=zf and pi == 0)
+                except GenerationError:
+                    text, fl, L = _ws_struct(model, alg, dt, int(tn["warps"]), K, trees=tuple(trees),
+                                             zero_fill=zf and pi == 0)
+                files[f"knots_{alg}_{dt}_{tag}.h"] = text
+                files[f"k_{alg}_{dt}_{tag}.cu"] = "\n".join([
+                    f'#include "knots_{alg}_{dt}_{tag}.h"',
+                    f'extern "C" int rbd__launch_{alg}_{dt}_{tag}(const void* q, const void* qd, const void* u,',
+                    "                                void* o0, void* o1, void* o2, int64_t N, void* stream) {",
+                    f"  return rbd_launch_kernel<{K}>(q, qd, u, o0, o1, o2, N, stream);",
+                    "}",
+                    "",
+                ])
+                ptags.append(tag)
             sig = "(const void*, const void*, const void*, void*, void*, void*, int64_t, void*);"
             for mp in maps:
                 dispatch.append(f'extern "C" int rbd__launch_{alg}_{dt}_{"W" if mp == "ws" else "T"}{sig}')
-            if maps == ["thread", "ws"] or maps == ["ws", "thread"]:
-                pick = (f"N <= {int(tn['ws_max_n'])} ? rbd__launch_{alg}_{dt}_W(q, qd, u, o0, o1, o2, N, stream)"
-                        f" : rbd__launch_{alg}_{dt}_T(q, qd, u, o0, o1, o2, N, stream)")
+            for tag in ptags:
+                dispatch.append(f'extern "C" int rbd__launch_{alg}_{dt}_{tag}{sig}')
+            args = "(q, qd, u, o0, o1, o2, N, stream)"
+            if ptags:
+                seq = " ".join(f"if ((rc = rbd__launch_{alg}_{dt}_{t}{args}) != 0) return rc;" for t in ptags)
+                zs = ""
+                if not zf and alg in ("Minv", "gradID", "gradFD"):
+                    es = 8 if dt == "f64" else 4
+                    zs = f"if ((rc = (int)cudaMemsetAsync(o0, 0, (size_t)N * {n * n * es}, (cudaStream_t)stream)) != 0) return rc; "
+                    if alg != "Minv":
+                        zs += f"if ((rc = (int)cudaMemsetAsync(o1, 0, (size_t)N * {n * n * es}, (cudaStream_t)stream)) != 0) return rc; "
+                big = f"[&]() {{ int rc; {zs}{seq} return 0; }}()"
             else:
-                pick = f"rbd__launch_{alg}_{dt}_{'W' if maps[0] == 'ws' else 'T'}(q, qd, u, o0, o1, o2, N, stream)"
+                big = f"rbd__launch_{alg}_{dt}_{'T' if 'thread' in maps else 'W'}{args}"
+            if "ws" in maps and (ptags or "thread" in maps):
+                pick = f"N <= {int(tn['ws_max_n'])} ? rbd__launch_{alg}_{dt}_W{args} : {big}"
+            elif ptags:
+                pick = big
+            else:
+                pick = f"rbd__launch_{alg}_{dt}_{'W' if maps[0] == 'ws' else 'T'}{args}"
             dispatch += [
                 f'extern "C" int rbd__launch_{alg}_{dt}(const void* q, const void* qd, const void* u,',
                 "                                void* o0, void* o1, void* o2, int64_t N, void* stream) {",

@@ -55,6 +55,22 @@ RBD_HD float rbd_fma(float a, float b, float c) { return fmaf(a, b, c); }
 // ---------------------------------------------------------------------------
 // batch kernel: CTA = BK knots, thread t = knot (blockIdx.x * BK + t)
 // ---------------------------------------------------------------------------
+// parked-output list length / identity flag (PARK kernels only)
+template <class K, class = void>
+struct rbd_park_traits {
+  static constexpr int nout = 0;
+  static constexpr bool ofull = true;
+};
+template <class K>
+struct rbd_park_traits<K, decltype((void)K::NOUT, void())> {
+  static constexpr int nout = K::NOUT;
+  static constexpr bool ofull = K::OFULL;
+};
+template <class K>
+__host__ __device__ constexpr int rbd_nout() { return rbd_park_traits<K>::nout; }
+template <class K>
+__host__ __device__ constexpr bool rbd_ofull() { return rbd_park_traits<K>::ofull; }
+
 template <class K>
 __global__ void __launch_bounds__(K::BK, K::MINB)
 rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __restrict__ qd,
@@ -70,31 +86,37 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
   const int nk = left < BK ? (int)left : BK;
   const int tid = threadIdx.x;
 
-  // all NIN * n loads of this thread are issued before the first smem store
-  // (one HBM round trip per CTA, not one per element)
-  T v[K::NIN][n];
+  // all NIN * NP loads of this thread are issued before the first smem store
+  // (one HBM round trip per CTA, not one per element); a part program reads
+  // only its dof window [LO, LO + NP) of each knot's inputs
+  constexpr int NP = K::NP;
+  T v[K::NIN][NP];
 #pragma unroll
   for (int a = 0; a < K::NIN; ++a) {
-    const T* src = (a == 0 ? q : (a == 1 ? qd : u)) + base * n;
+    const T* src = (a == 0 ? q : (a == 1 ? qd : u)) + base * n + K::LO;
 #pragma unroll
-    for (int r = 0; r < n; ++r) {
+    for (int r = 0; r < NP; ++r) {
       const int idx = tid + r * BK;
-      v[a][r] = (idx < nk * n) ? __ldg(src + idx) : T(0);
+      const int k = idx / NP, j = idx - k * NP;
+      v[a][r] = (idx < nk * NP) ? __ldg(src + k * n + j) : T(0);
     }
   }
 #pragma unroll
   for (int a = 0; a < K::NIN; ++a) {
 #pragma unroll
-    for (int r = 0; r < n; ++r) {
+    for (int r = 0; r < NP; ++r) {
       const int idx = tid + r * BK;
-      const int k = idx / n, j = idx - k * n;
-      s_in[k * K::SIN + a * n + j] = v[a][r];
+      const int k = idx / NP, j = idx - k * NP;
+      s_in[k * K::SIN + a * NP + j] = v[a][r];
     }
   }
-  constexpr int EALL = K::E0 + K::E1 + K::E2;
-  short* s_map = reinterpret_cast<short*>(s_in + BK * K::SIN);  // PARK: output element -> row slot
+  short* s_map = reinterpret_cast<short*>(s_in + BK * K::SIN);  // PARK: output list -> row slot
+  unsigned short* s_elem = reinterpret_cast<unsigned short*>(s_map + rbd_nout<K>());
   if constexpr (K::PARK) {
-    for (int e = tid; e < EALL; e += BK) s_map[e] = K::omap()[e];
+    for (int j = tid; j < rbd_nout<K>(); j += BK) {
+      s_map[j] = K::omap()[j];
+      if constexpr (!rbd_ofull<K>()) s_elem[j] = K::oelem()[j];
+    }
   }
   __syncthreads();
   T* my = s_in + tid * K::SIN;  // this knot's inputs + its sin/cos scratch
@@ -104,6 +126,21 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
     // contiguous output ranges back coalesced (structural zeros from the map)
     K::run_dev(my, nullptr, nullptr, nullptr, 1u);
     __syncthreads();
+    if constexpr (!rbd_ofull<K>()) {
+      // a part program (subset of the root trees): only its own elements
+      constexpr int M = rbd_nout<K>();
+      for (int idx = tid; idx < nk * M; idx += BK) {
+        const int k = idx / M, j = idx - k * M;
+        const int e = s_elem[j], sl = s_map[j];
+        const T v = sl >= 0 ? s_in[k * K::SIN + sl] : T(0);
+        if (e < K::E0)
+          __stcs(o0 + (base + k) * K::E0 + e, v);
+        else if (e < K::E0 + K::E1)
+          __stcs(o1 + (base + k) * K::E1 + (e - K::E0), v);
+        else
+          __stcs(o2 + (base + k) * K::E2 + (e - K::E0 - K::E1), v);
+      }
+    } else
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
       const int E = b == 0 ? K::E0 : (b == 1 ? K::E1 : K::E2);
@@ -175,15 +212,16 @@ rbd_ws_kernel(const typename K::T* __restrict__ q, const typename K::T* __restri
   for (long long g = blockIdx.x; g < groups; g += gridDim.x) {
     const long long base = g * 32;
     const int nk = (N - base) < 32 ? (int)(N - base) : 32;
-    constexpr int PER = (32 * n + NT - 1) / NT;  // loads per thread per input
+    constexpr int NP = K::NP, PER = (32 * NP + NT - 1) / NT;  // loads per thread per input
     T v[K::NIN][PER];
 #pragma unroll
     for (int a = 0; a < K::NIN; ++a) {
-      const T* src = (a == 0 ? q : (a == 1 ? qd : u)) + base * n;
+      const T* src = (a == 0 ? q : (a == 1 ? qd : u)) + base * n + K::LO;
 #pragma unroll
       for (int r = 0; r < PER; ++r) {
         const int idx = tid + r * NT;
-        v[a][r] = (idx < nk * n) ? __ldg(src + idx) : T(0);
+        const int k = idx / NP, j = idx - k * NP;
+        v[a][r] = (idx < nk * NP) ? __ldg(src + k * n + j) : T(0);
       }
     }
 #pragma unroll
@@ -191,9 +229,9 @@ rbd_ws_kernel(const typename K::T* __restrict__ q, const typename K::T* __restri
 #pragma unroll
       for (int r = 0; r < PER; ++r) {
         const int idx = tid + r * NT;
-        if (idx < 32 * n) {
-          const int k = idx / n, j = idx - k * n;
-          s_in[(a * n + j) * L + k] = v[a][r];
+        if (idx < 32 * NP) {
+          const int k = idx / NP, j = idx - k * NP;
+          s_in[(a * NP + j) * L + k] = v[a][r];
         }
       }
     }
@@ -252,7 +290,7 @@ constexpr size_t rbd_smem_bytes() {
            (K::SIN + (K::ARENA_SMEM ? K::NA : 0) + (K::STAGE ? K::SOUT : 0));
   else
     return sizeof(typename K::T) * (size_t)K::BK * (K::SIN + (K::STAGE ? K::SOUT : 0)) +
-           (K::PARK ? sizeof(short) * (size_t)(K::E0 + K::E1 + K::E2) : 0);
+           sizeof(short) * (size_t)rbd_nout<K>() * (rbd_ofull<K>() ? 1 : 2);
 }
 
 // per-device cache of (CTAs per SM x SMs) and of the global arena
