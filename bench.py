@@ -187,6 +187,7 @@ def fma_peak_tflops(torch, dtype):
     st = torch.cuda.current_stream()
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     blocks, iters = sms * 8, 4096
+    per_iter = 2 * 16
     for _ in range(3):
         lib.rbd_fma_peak(1 if dtype == "f64" else 0, blocks, iters, sink.data_ptr(), st.cuda_stream)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -196,7 +197,7 @@ def fma_peak_tflops(torch, dtype):
         lib.rbd_fma_peak(1 if dtype == "f64" else 0, blocks, iters, sink.data_ptr(), st.cuda_stream)
         e1.record(st)
         e1.synchronize()
-        best = max(best, 2.0 * 16 * iters * 256 * blocks / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+        best = max(best, float(per_iter) * iters * 256 * blocks / (e0.elapsed_time(e1) * 1e-3) / 1e12)
     return best
 
 
@@ -305,13 +306,21 @@ def run_ours(args):
     achieved = flops_ref * N / (ms * 1e-3) / 1e12 if flops_ref else None
     es = 8 if dt == "f64" else 4
     alg_bytes = (h2d + d2h)  # compulsory HBM bytes per launch = inputs + outputs
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if os.path.exists(prof):
+    traffic, traffic_src = None, None
+    # dram__bytes_read+write per launch of this kernel from the newest committed
+    # `ncu --set full` capture (profiles/ncu_summary_r<k>.json)
+    import glob
+    import re
+    profs = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_summary_r*.json")),
+                   key=lambda f: int(re.search(r"_r(\d+)", f).group(1)))
+    for prof in reversed(profs):
         try:
-            traffic = json.load(open(prof)).get(f"{robot}_{alg}_{dt}", {}).get("dram_bytes_per_launch")
+            t = json.load(open(prof)).get(f"{robot}_{alg}_{dt}", {}).get("dram_bytes_per_launch")
         except Exception:
-            traffic = None
+            t = None
+        if t:
+            traffic, traffic_src = t * N / (1 << 20), os.path.relpath(prof, ROOT)
+            break
 
     result = {
         "metric": f"dFD knot-points/sec ({PAPER.get(robot, robot)} stand-in {robot}, {alg}, N={N}/GPU)",
@@ -334,13 +343,14 @@ def run_ours(args):
                 "ms_per_step": e2e_s * 1e3, "path": "rbd_run_host (C ABI, pinned host buffers)"},
         "roofline": {"bound": "fp64" if dt == "f64" else "fp32", "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
-                     "traffic": traffic, "algorithmic_bytes": alg_bytes,
+                     "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes": alg_bytes,
                      "hbm_gbs": alg_bytes / (ms * 1e-3) / 1e9,
                      "hbm_frac": alg_bytes / (ms * 1e-3) / 1e9 / _hbm_peak(),
                      "flops_per_knot_ref_ir": flops_ref, "flops_per_knot_kernel": flops_ours,
                      "hw_frac": (flops_ours * N / (ms * 1e-3) / 1e12 / peak) if flops_ours else None,
-                     "peak_source": "measured in this run: rbd_peak.cu fp64/fp32 FMA loop "
-                                    "(MEASURED_PEAKS.json has no CUDA-core FP peak)",
+                     "peak_source": "measured in this run: rbd_peak.cu, 16 independent fp64/fp32 FMA chains "
+                                    "per thread, 64 warps/SM (nominal B200 at 1965 MHz: 37.2 TF fp64, 74.4 TF "
+                                    "fp32; MEASURED_PEAKS.json has no CUDA-core FP peak)",
                      "peak_fp64_tflops": peak64, "peak_fp32_tflops": peak32},
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
@@ -410,11 +420,11 @@ def run_reference(args):
     if rank != 0:
         return
     cores = host_cores()
-    sample = args.cpu_sample
+    sample = max(cores, args.cpu_sample // 4)  # per step: ~3 s of CPU work on 16 cores
     rates = []
-    for _ in range(args.warmup and 1):
-        cpu_reference_rate(args.robot, args.alg, min(sample, cores * 4), cores)
-    for _ in range(max(1, min(args.steps, 3))):
+    for _ in range(args.warmup):
+        cpu_reference_rate(args.robot, args.alg, cores * 4, cores)
+    for _ in range(max(1, args.steps)):
         rates.append(cpu_reference_rate(args.robot, args.alg, sample, cores)[0])
     value = statistics.median(rates)
     print(json.dumps({
@@ -422,7 +432,7 @@ def run_reference(args):
         "metric": f"dFD knot-points/sec ({PAPER.get(args.robot, args.robot)} stand-in {args.robot}, "
                   f"{args.alg}, N={args.n}/GPU)",
         "value": value, "unit": "knots/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
-        "steps": len(rates), "warmup": 1, "higher_is_better": True, "scaling": "weak",
+        "steps": len(rates), "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic seeded states (SURVEY 8d, seed 1)",
         "config": {"workload": f"{args.robot} {args.alg} f64, N={args.n} knots per GPU "
                                f"(CPU: bounded sample of {sample} knots per step)",
@@ -443,7 +453,8 @@ def main():
     ap.add_argument("--alg", default="gradFD")
     ap.add_argument("--dtype", default="f64", choices=("f64", "f32"))
     ap.add_argument("--n", type=int, default=1 << 20)
-    ap.add_argument("--cpu-sample", type=int, default=4096)
+    ap.add_argument("--cpu-sample", type=int, default=65536,
+                    help="knots per CPU-baseline sample (~10-20 s of work on a 16-core host)")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
