@@ -116,6 +116,14 @@ int rbd_session_destroy(rbd_session* s);
 int rbd_run_host(rbd_session* s, int alg, int dtype, const void* q, const void* qd,
                  const void* u, void* out0, void* out1, void* out2, int64_t N);
 
+/* Benchmark helper (not in the reference interface): calls rbd_run_host
+ * `reps` times back to back and stores the mean host wall time per call in
+ * *seconds (steady clock) -- the end-to-end latency a C/C++ caller sees,
+ * without any binding-language overhead. */
+int rbd_bench_host(rbd_session* s, int alg, int dtype, const void* q, const void* qd,
+                   const void* u, void* out0, void* out1, void* out2, int64_t N, int32_t reps,
+                   double* seconds);
+
 #ifdef __cplusplus
 }
 #endif

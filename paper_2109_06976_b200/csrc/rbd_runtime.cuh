@@ -20,6 +20,9 @@
 #include <stdint.h>
 #include <string.h>
 #include <math.h>
+#if defined(__CUDACC__)
+#include <chrono>
+#endif
 
 #include "rbd_b200.h"
 
@@ -575,6 +578,20 @@ extern "C" int rbd_run_host(rbd_session* s, int alg, int dtype, const void* q, c
   }
   cudaSetDevice(prev);
   return rc;
+}
+
+extern "C" int rbd_bench_host(rbd_session* s, int alg, int dtype, const void* q, const void* qd,
+                              const void* u, void* out0, void* out1, void* out2, int64_t N,
+                              int32_t reps, double* seconds) {
+  if (!seconds || reps <= 0) return RBD_EINVAL;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int32_t r = 0; r < reps; ++r) {
+    const int rc = rbd_run_host(s, alg, dtype, q, qd, u, out0, out1, out2, N);
+    if (rc) return rc;
+  }
+  const auto t1 = std::chrono::steady_clock::now();
+  *seconds = std::chrono::duration<double>(t1 - t0).count() / reps;
+  return 0;
 }
 #endif  // RBD_MAIN_TU
 

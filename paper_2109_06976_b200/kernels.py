@@ -142,7 +142,7 @@ class RbdInfo(ctypes.Structure):
 
 
 ABI_SYMBOLS = (["rbd_get_info", "rbd_alg_extents", "rbd_launch", "rbd_session_create",
-                "rbd_session_destroy", "rbd_run_host"]
+                "rbd_session_destroy", "rbd_run_host", "rbd_bench_host"]
                + [f"rbd_{a}_{d}" for a in codegen.ALGORITHMS for d in codegen.DTYPES])
 
 _vp = ctypes.c_void_p
@@ -155,6 +155,8 @@ def _bind(lib):
     lib.rbd_session_create.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(_vp)]
     lib.rbd_session_destroy.argtypes = [_vp]
     lib.rbd_run_host.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64]
+    lib.rbd_bench_host.argtypes = ([_vp, ctypes.c_int, ctypes.c_int] + [_vp] * 6
+                                   + [ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)])
     for a in codegen.ALGORITHMS:
         for d in codegen.DTYPES:
             fn = getattr(lib, f"rbd_{a}_{d}")

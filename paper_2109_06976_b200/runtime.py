@@ -69,6 +69,17 @@ class Session:
         rc = self.lib.rbd_run_host(self.handle, _ALG_ID[alg], _DT_ID[dtype], *ins, *outs, ctypes.c_int64(N))
         check(rc, f"rbd_run_host({alg}, {dtype})")
 
+    def bench(self, alg, dtype, in_arrays, out_arrays, N, reps):
+        """Mean wall seconds per rbd_run_host call, timed inside the library
+        (rbd_bench_host: the latency a C/C++ caller sees)."""
+        ins = [a.ctypes.data_as(ctypes.c_void_p) for a in in_arrays] + [None] * (3 - len(in_arrays))
+        outs = [a.ctypes.data_as(ctypes.c_void_p) for a in out_arrays] + [None] * (3 - len(out_arrays))
+        sec = ctypes.c_double()
+        rc = self.lib.rbd_bench_host(self.handle, _ALG_ID[alg], _DT_ID[dtype], *ins, *outs, ctypes.c_int64(N),
+                                     int(reps), ctypes.byref(sec))
+        check(rc, f"rbd_bench_host({alg}, {dtype})")
+        return sec.value
+
     def close(self):
         if self.handle:
             self.lib.rbd_session_destroy(self.handle)

@@ -278,6 +278,8 @@ def plan(model, alg, dtype, warps, trees=None, zero_fill=True):
     row = LANES * es
     sout = sum(ext)
     opts = [(True, True), (True, False), (False, True), (False, False)]  # (arena smem, stage outputs)
+    if cg.tuning(model, alg, dtype).get("arena") == "global":
+        opts = [(False, True), (False, False)]
     for ar, st in opts:
         smem = row * (sin + (sched.nslots if ar else 0) + (sout if st else 0))
         if smem <= SMEM_BUDGET:

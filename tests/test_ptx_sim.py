@@ -120,3 +120,98 @@ def test_ws_humanoid30_gradfd_one_knot():
     outs, _ = run_ws(m, "gradFD", "f64", x, warps=16, arena_space="global", out_space="global")
     for (nm, _), o in zip(codegen.outputs("gradFD", m.n_dof), outs):
         assert rel_err(o[None], g[f"gradFD.{nm}"][2:3]) < 1e-12
+
+
+def _run_part(model, alg, x_full, trees, zero_fill, budget):
+    """One part program (a subset of root trees, inputs from its dof window),
+    as the large-batch kernel runs it: planned registers, parked outputs."""
+    em = codegen.generate_knot(model, alg, "f64", trees, zero_fill)
+    n = model.n_dof
+    nin = len(codegen.INPUTS[alg])
+    lo, np_ = em.lo, em.np
+    x = np.concatenate([x_full[a * n + lo:a * n + lo + np_] for a in range(nin)])
+    nsc = len(_sincos_slots(em))
+    plan = codegen.SpillPlan(em, budget, codegen.row_homes(em, nin * np_), nin * np_ + 2 * nsc, park_outputs=True)
+    ctab = codegen.ConstTable("K", "f64")
+    lines, sc = codegen.ptx_body(em, nin * np_, "global", ctab=ctab, plan=plan)
+    row = {i: float(v) for i, v in enumerate(x)}
+    for k, slot in enumerate(sc):
+        row[nin * np_ + 2 * k] = math.sin(x[slot])
+        row[nin * np_ + 2 * k + 1] = math.cos(x[slot])
+    ptxsim.run_block(lines, [row, {}, {}, {}, None], [8] * 5, consts={"K": sorted(ctab.index, key=ctab.index.get)})
+    outs = [dict() for _ in range(3)]
+    for (k, idx), sl in plan.outslot.items():
+        outs[k][idx] = row[sl]
+    for (k, idx), v in plan.outconst.items():
+        outs[k][idx] = v
+    return outs
+
+
+@pytest.mark.parametrize("name", ["quad12", "humanoid30"])
+def test_part_programs_compose_to_the_whole(name):
+    """The large-batch path runs one program per root tree (part 0 also
+    writes the cross-part zeros); together they must reproduce the reference
+    exactly, each part touching only its own output elements."""
+    g = golden(name)
+    m = models.load(name)
+    n = m.n_dof
+    trees = list(range(len(m.roots())))
+    for alg in ("FD", "gradFD") if name == "humanoid30" else codegen.ALGORITHMS:
+        x = _inputs(g, alg, 1, n)
+        merged = [dict() for _ in range(3)]
+        for t in trees:
+            if name == "humanoid30" and t == 0 and alg == "gradFD":
+                continue  # the torso part runs warp-specialised (covered on the GPU)
+            outs = _run_part(m, alg, x, (t,), t == 0, 64)
+            owned = set(m.subtree(m.roots()[t]))
+            for k, o in enumerate(outs):
+                for idx, v in o.items():
+                    # only part 0's structural zeros may be overwritten (the parts run in order)
+                    assert idx not in merged[k] or merged[k][idx] == 0.0, (alg, t, k, idx)
+                    if len(o) and codegen.outputs(alg, n)[k][1] == n * n and v != 0.0:
+                        assert idx // n in owned and idx % n in owned
+                    merged[k][idx] = v
+        for (nm, e), o in zip(codegen.outputs(alg, n), merged):
+            ref = g[f"{alg}.{nm}"][1]
+            got = np.array([o.get(i, np.nan) for i in range(e)])
+            if name == "humanoid30" and alg == "gradFD":
+                own = [i for i in range(e) if not np.isnan(got[i])]
+                assert rel_err(got[own][None], ref[own][None]) < 1e-12, (name, alg, nm)
+            else:
+                assert np.all(np.isfinite(got)), (name, alg, nm)
+                assert rel_err(got[None], ref[None]) < 1e-12, (name, alg, nm)
+
+
+def test_spill_plan_invariants():
+    """Register plan, replayed op by op: a reload finds its own value in the
+    slot, a slot is only overwritten once its previous value is dead, parked
+    outputs are never overwritten, slots are recycled, and a tighter budget
+    costs more reloads."""
+    m = models.load("chain7")
+    em = codegen.generate_knot(m, "gradFD", "f64")
+    homes = codegen.row_homes(em, 21)
+    last = {}
+    for i, op in enumerate(em.ops):
+        for r in codegen.op_srcs(op):
+            last[r] = i
+    for budget in (8, 40, 119):
+        plan = codegen.SpillPlan(em, budget, homes, 35, park_outputs=True)
+        owner = {sl: v for v, sl in homes.items()}
+        for i, op in enumerate(em.ops):
+            for a in plan.before.get(i, ()):
+                assert owner.get(plan.slot[a]) == a, (budget, i, a)
+            if op[0] == "st" and not isinstance(op[3], float):
+                sl = plan.outslot[(op[1], op[2])]
+                prev = owner.get(sl)
+                assert prev is None or (not isinstance(prev, tuple) and last.get(prev, -1) < i), (budget, i, prev)
+                owner[sl] = ("out", op[1], op[2])
+            for v, sl in plan.after.get(i, ()):
+                prev = owner.get(sl)
+                assert prev is None or (not isinstance(prev, tuple) and last.get(prev, -1) <= i), (budget, i, prev)
+                owner[sl] = v
+        parked = {v for v in owner.values() if isinstance(v, tuple)}
+        assert len(parked) == len(plan.outslot)
+        assert plan.nslots < 35 + plan.stores + len(plan.outslot)  # slots were recycled
+    tight = codegen.SpillPlan(em, 8, homes, 35)
+    loose = codegen.SpillPlan(em, 119, homes, 35)
+    assert tight.reloads > loose.reloads and loose.stores <= tight.stores
