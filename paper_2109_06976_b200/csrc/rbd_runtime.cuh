@@ -399,7 +399,7 @@ static inline size_t rbd_align256(size_t x) { return (x + 255) & ~(size_t)255; }
 // host memory directly over PCIe (zero-copy) -- one launch + one sync.
 // Caller buffers that are already pinned are used in place; pageable ones go
 // through the session's pinned staging area with host memcpy.
-#define RBD_ZC_BYTES (4u << 20)
+#define RBD_ZC_BYTES (1u << 20)
 struct rbd_session {
   int device;
   int64_t chunk;
