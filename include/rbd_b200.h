@@ -100,6 +100,33 @@ int rbd_gradFD_f32(const float* q, const float* qd, const float* tau, float* dq_
 int rbd_launch(int alg, int dtype, const void* q, const void* qd, const void* u,
                void* out0, void* out1, void* out2, int64_t N, void* stream);
 
+/* ---- external forces (refdyn's f_ext argument, refdyn.py:79-80, :91-249) ---
+ * f_ext[k*n*6 + i*6 + c]: spatial force [moment; force] on link i of knot k in
+ * link-i coordinates, subtracted from the link's Newton-Euler force (ID, FD,
+ * and both gradients, which hold f_ext fixed in the link frame).  Minv takes
+ * no f_ext. */
+int rbd_ID_f64_fext(const double* q, const double* qd, const double* qdd, const double* f_ext,
+                    double* tau_out, double* unused1, double* unused2, int64_t N, void* stream);
+int rbd_FD_f64_fext(const double* q, const double* qd, const double* tau, const double* f_ext,
+                    double* qdd_out, double* unused1, double* unused2, int64_t N, void* stream);
+int rbd_gradID_f64_fext(const double* q, const double* qd, const double* qdd, const double* f_ext,
+                        double* dq_out, double* dqd_out, double* unused2, int64_t N, void* stream);
+int rbd_gradFD_f64_fext(const double* q, const double* qd, const double* tau, const double* f_ext,
+                        double* dq_out, double* dqd_out, double* qdd_out, int64_t N, void* stream);
+int rbd_ID_f32_fext(const float* q, const float* qd, const float* qdd, const float* f_ext,
+                    float* tau_out, float* unused1, float* unused2, int64_t N, void* stream);
+int rbd_FD_f32_fext(const float* q, const float* qd, const float* tau, const float* f_ext,
+                    float* qdd_out, float* unused1, float* unused2, int64_t N, void* stream);
+int rbd_gradID_f32_fext(const float* q, const float* qd, const float* qdd, const float* f_ext,
+                        float* dq_out, float* dqd_out, float* unused2, int64_t N, void* stream);
+int rbd_gradFD_f32_fext(const float* q, const float* qd, const float* tau, const float* f_ext,
+                        float* dq_out, float* dqd_out, float* qdd_out, int64_t N, void* stream);
+
+/* Generic form of the eight f_ext entries (alg != RBD_MINV). */
+int rbd_launch_fext(int alg, int dtype, const void* q, const void* qd, const void* u,
+                    const void* f_ext, void* out0, void* out1, void* out2, int64_t N,
+                    void* stream);
+
 /* ---- host-buffer entries (end-to-end path) -------------------------------- */
 typedef struct rbd_session rbd_session;
 
@@ -115,6 +142,11 @@ int rbd_session_destroy(rbd_session* s);
  * returns after the last D2H has landed. */
 int rbd_run_host(rbd_session* s, int alg, int dtype, const void* q, const void* qd,
                  const void* u, void* out0, void* out1, void* out2, int64_t N);
+
+/* rbd_run_host with per-link external forces (host buffer, layout as above). */
+int rbd_run_host_fext(rbd_session* s, int alg, int dtype, const void* q, const void* qd,
+                      const void* u, const void* f_ext, void* out0, void* out1, void* out2,
+                      int64_t N);
 
 /* Benchmark helper (not in the reference interface): calls rbd_run_host
  * `reps` times back to back and stores the mean host wall time per call in

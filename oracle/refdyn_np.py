@@ -306,32 +306,35 @@ def finite_diff(fn, x, h):
 ALGORITHMS = ("ID", "Minv", "FD", "gradID", "gradFD")
 
 
-def evaluate(model, alg, q, qd=None, u=None):
+def evaluate(model, alg, q, qd=None, u=None, f_ext=None):
     """One knot of `alg`; returns {output name: flat array} like
-    `interp.interpret` (reference `interp.py:83-86`)."""
+    `interp.interpret` (reference `interp.py:83-86`).  f_ext: (n, 6) per-link
+    external forces as refdyn takes them (refdyn.py:79-80)."""
     if alg == "ID":
-        return {"tau_out": rnea(model, q, qd, u)}
+        return {"tau_out": rnea(model, q, qd, u, f_ext)}
     if alg == "Minv":
         return {"minv_out": minv_direct(model, q).ravel()}
     if alg == "FD":
-        return {"qdd_out": forward_dynamics(model, q, qd, u)}
+        return {"qdd_out": forward_dynamics(model, q, qd, u, f_ext)}
     if alg == "gradID":
-        dq, dqd = rnea_grad(model, q, qd, u)
+        dq, dqd = rnea_grad(model, q, qd, u, f_ext)
         return {"dq_out": dq.ravel(), "dqd_out": dqd.ravel()}
     if alg == "gradFD":
         Mi = minv_direct(model, q)
-        qdd = Mi @ (np.asarray(u, dtype=float) - bias_force(model, q, qd))
-        dq, dqd = rnea_grad(model, q, qd, qdd)
+        qdd = Mi @ (np.asarray(u, dtype=float) - bias_force(model, q, qd, f_ext))
+        dq, dqd = rnea_grad(model, q, qd, qdd, f_ext)
         return {"dq_out": (-Mi @ dq).ravel(), "dqd_out": (-Mi @ dqd).ravel(), "qdd_out": qdd}
     raise ValueError(f"unknown algorithm {alg!r}")
 
 
-def evaluate_batch(model, alg, q, qd=None, u=None):
-    """Loop `evaluate` over the leading knot axis; returns {name: (N, extent)}."""
+def evaluate_batch(model, alg, q, qd=None, u=None, f_ext=None):
+    """Loop `evaluate` over the leading knot axis; returns {name: (N, extent)}.
+    f_ext: (N, n, 6) or None."""
     N = q.shape[0]
     outs = None
     for k in range(N):
-        r = evaluate(model, alg, q[k], None if qd is None else qd[k], None if u is None else u[k])
+        r = evaluate(model, alg, q[k], None if qd is None else qd[k], None if u is None else u[k],
+                     None if f_ext is None else np.asarray(f_ext[k]).reshape(-1, 6))
         if outs is None:
             outs = {nm: np.zeros((N,) + np.shape(v)) for nm, v in r.items()}
         for nm, v in r.items():

@@ -53,6 +53,23 @@ INPUTS = {
 }
 
 
+# algorithms whose reference entry takes f_ext (refdyn.py:91-249; minv_direct has none)
+FEXT_ALGORITHMS = ("ID", "FD", "gradID", "gradFD")
+
+
+def input_names(alg, fext=False):
+    """Per-knot inputs of a program: the reference operator inputs, plus the
+    per-link external forces f_ext [n][6] (link coordinates, refdyn.py:79-80)."""
+    if fext and alg not in FEXT_ALGORITHMS:
+        raise GenerationError(f"{alg} takes no f_ext")
+    return INPUTS[alg] + (("f_ext",) if fext else ())
+
+
+def input_width(name):
+    """Scalars per dof of an input (q, qd, qdd/tau: 1; f_ext: 6)."""
+    return 6 if name == "f_ext" else 1
+
+
 def outputs(alg, n):
     """[(name, extent)] in output_map order."""
     return {
@@ -115,6 +132,9 @@ class _Emit:
         self.nreg = 0
         self.flops = 0  # FMA = 2, MUL/ADD/SUB/RCP = 1 (the reference's counting rule)
         self.lo, self.np = 0, 0  # input dof window of the program (set by _Program.run)
+        self.in_layout = []      # [(name, row offset, window length, global offset, global stride)]
+        self.in_total = 0        # row slots taken by the inputs
+        self.fext = False
 
     def reg(self):
         self.nreg += 1
@@ -319,12 +339,23 @@ class _Program:
     # -- inputs and joint transforms -------------------------------------------
     def load_inputs(self, names):
         """Per-knot input row: the program's dof window [lo, lo + np) of each
-        input, q at slots [0, np), qd at [np, 2np), u at [2np, 3np)."""
+        input, q at slots [0, np), qd at [np, 2np), u at [2np, 3np), then
+        f_ext (6 per dof) when present."""
         em = self.em
-        lo, np_ = em.lo, em.np
+        lo, np_, n = em.lo, em.np, self.n
         self.inp = {}
-        for a, nm in enumerate(names):
-            self.inp[nm] = [em.load(a * np_ + i - lo) if lo <= i < lo + np_ else None for i in range(self.n)]
+        off = 0
+        em.in_layout = []
+        for nm in names:
+            w = input_width(nm)
+            em.in_layout.append((nm, off, w * np_, w * lo, w * n))
+            if w == 1:
+                self.inp[nm] = [em.load(off + i - lo) if lo <= i < lo + np_ else None for i in range(n)]
+            else:
+                self.inp[nm] = [[em.load(off + w * (i - lo) + k) for k in range(w)] if lo <= i < lo + np_ else None
+                                for i in range(n)]
+            off += w * np_
+        em.in_total = off
 
     def emit_xform(self, i):
         """X_i = [[E, 0], [-E skew(r), E]] as an entry grid (folded)."""
@@ -413,7 +444,10 @@ class _Program:
                 mcross_t(v[i], vJ[i], rows)
             a[i] = em.vec(rows, hint="a")
             Iv[i] = em.vec(mv_t(self.I[i], v[i]), hint="iv")
-            f[i] = em.vec(fcross_t(v[i], Iv[i], mv_t(self.I[i], a[i])), hint="f")
+            rows = fcross_t(v[i], Iv[i], mv_t(self.I[i], a[i]))
+            if em.fext:
+                add_t(rows, self.inp["f_ext"][i], -1.0)  # f_i -= f_ext_i (refdyn.py:79-80)
+            f[i] = em.vec(rows, hint="f")
         tau = {}
         for i in reversed(tree):
             tau[i] = em.lin([(1.0, f[i][r], self.S[i][r]) for r in range(6)], hint="tau")
@@ -562,7 +596,7 @@ class _Program:
     def store(self, slot, idx, e):
         self.em.store(int(slot[1]), idx, e)
 
-    def run(self, trees=None, zero_fill=True, cols=None):
+    def run(self, trees=None, zero_fill=True, cols=None, fext=False):
         """Emit the whole one-knot program.  Every op carries a task tag:
         'in' / 'xf' (input loads, joint transforms: re-materialised by each
         consumer), then per root tree t: rnea0.t, ia.t, minv.t.j, fd.t,
@@ -574,8 +608,9 @@ class _Program:
         if not dofs or dofs != list(range(dofs[0], dofs[-1] + 1)):
             raise GenerationError(f"part {trees}: its trees must cover a contiguous dof range")
         em.lo, em.np = dofs[0], len(dofs)
+        em.fext = bool(fext)
         em.task = "in"
-        self.load_inputs(INPUTS[alg])
+        self.load_inputs(input_names(alg, fext))
         em.task = "xf"
         for i in range(n):
             if any(i in self.trees[t] for t in part):
@@ -744,11 +779,11 @@ def stage_outputs(model, alg, dtype, bk):
     return bk * _odd(ext) * es <= tuning(model, alg, dtype)["stage_kb"] * 1024
 
 
-def generate_knot(model, alg, dtype, trees=None, zero_fill=True, cols=None):
+def generate_knot(model, alg, dtype, trees=None, zero_fill=True, cols=None, fext=False):
     """The one-knot program as an op list (`_Emit`).  trees: restrict to
     these root trees (a 'part'; its outputs are the trees' blocks);
     zero_fill: also store the structural zeros outside the blocks emitted."""
-    return _Program(model, alg, dtype).run(trees, zero_fill, None if cols is None else frozenset(cols))
+    return _Program(model, alg, dtype).run(trees, zero_fill, None if cols is None else frozenset(cols), fext)
 
 
 def _lit(x, dtype):
@@ -795,6 +830,14 @@ class ConstTable:
         return [f'__constant__ double {self.symbol}[{len(vals)}] = {{{body}}};']
 
 
+def _input_of_slot(em, slot):
+    """(host array name, index within the knot's full input row) of a row slot."""
+    for a, (nm, off, w, goff, _) in enumerate(em.in_layout):
+        if off <= slot < off + w:
+            return ("iq", "iqd", "iu", "ifx")[a], goff + slot - off
+    raise GenerationError(f"slot {slot} is not an input")
+
+
 def cpp_body(em, n):
     """Host C++ backend (test harness only): one statement per op."""
     lit = lambda a: _lit(a, em.dtype) if isinstance(a, float) else f"r{a}"
@@ -802,7 +845,8 @@ def cpp_body(em, n):
     for op in em.ops:
         k = op[0]
         if k == "ld":
-            out.append(f"const T r{op[1]} = {('iq', 'iqd', 'iu')[op[2] // em.np]}[{em.lo + op[2] % em.np}];")
+            arr, idx = _input_of_slot(em, op[2])
+            out.append(f"const T r{op[1]} = {arr}[{idx}];")
         elif k == "sincos":
             out.append(f"T r{op[1]}, r{op[2]}; rbd_sincos(iq[{em.lo + op[3]}], &r{op[1]}, &r{op[2]});")
         elif k == "fma":
@@ -1089,16 +1133,16 @@ def _layout(model, alg, dt, em, device=True):
     n = model.n_dof
     outs = outputs(alg, n)
     ext = [e for _, e in outs] + [0] * (3 - len(outs))
-    nin = len(INPUTS[alg])
+    nin = len(em.in_layout)
     nsc = sum(1 for op in em.ops if op[0] == "sincos")
     tn = tuning(model, alg, dt)
     bk = int(tn["bk"])
     es = 8 if dt == "f64" else 4
-    base = nin * em.np + 2 * nsc
+    base = em.in_total + 2 * nsc
     sout = _odd(sum(ext))
     plan, minb = None, 1
     if tn.get("ra") and device:
-        homes = row_homes(em, nin * em.np)
+        homes = row_homes(em, em.in_total)
         for warps in range(int(tn["warps_per_sm"]), 1, -1):
             threads = 32 * warps
             if threads % bk:
@@ -1124,7 +1168,16 @@ def _layout(model, alg, dt, em, device=True):
         row = _odd(base)
         stage = stage_outputs(model, alg, dt, bk)
     return dict(n=n, ext=ext, nin=nin, nsc=nsc, bk=bk, stage=stage, sin=row, sout=sout,
-                plan=plan, minb=minb, park=plan is not None, lo=em.lo, np=em.np)
+                plan=plan, minb=minb, park=plan is not None, lo=em.lo, np=em.np, in_layout=em.in_layout)
+
+
+def _input_consts(layout):
+    """Per-input staging constants of a kernel struct: window length, offset
+    and stride in the knot's global row, offset in the knot's smem row."""
+    def fn(name, idx):
+        body = " : ".join(f"a == {a} ? {ent[idx]}" for a, ent in enumerate(layout)) + " : 0"
+        return f"  RBD_HDC static constexpr int {name}(int a) {{ return {body}; }}"
+    return [fn("inw", 2), fn("ing", 3), fn("ins", 4), fn("inr", 1)]
 
 
 def _struct_head(model, alg, dt, L, fl, name=None):
@@ -1134,6 +1187,7 @@ def _struct_head(model, alg, dt, L, fl, name=None):
         f"  typedef {T} T;",
         f"  static constexpr int NDOF = {L['n']}, NIN = {L['nin']}, BK = {L['bk']};",
         f"  static constexpr int LO = {L['lo']}, NP = {L['np']};  // input dof window [LO, LO + NP)",
+    ] + _input_consts(L["in_layout"]) + [
         f"  static constexpr int E0 = {L['ext'][0]}, E1 = {L['ext'][1]}, E2 = {L['ext'][2]};",
         f"  static constexpr int SIN = {L['sin']}, SOUT = {L['sout']};",
         f"  static constexpr bool STAGE = {'true' if L['stage'] else 'false'};",
@@ -1178,16 +1232,16 @@ def _omap_decl(L, name):
     return lines
 
 
-def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True):
+def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=False):
     """Device header: C++ sin/cos prologue + the PTX body in one asm block."""
-    em = generate_knot(model, alg, dt, trees, zero_fill)
+    em = generate_knot(model, alg, dt, trees, zero_fill, fext=fext)
     L = _layout(model, alg, dt, em)
     n = L["n"]
     space = "shared" if L["stage"] else "global"
     tn = tuning(model, alg, dt)
     ctab = ConstTable(f"rbd_c_{name or f'Knot_{alg}_{dt}'}", dt)
     plan = L["plan"]
-    body, sc = ptx_body(em, L["nin"] * em.np, space, tn["sync_every"], tn["reload_dist"], ctab, plan)
+    body, sc = ptx_body(em, em.in_total, space, tn["sync_every"], tn["reload_dist"], ctab, plan)
     ra = (f"// register budget: {plan.reloads} reloads, {plan.stores} parked values, row {L['sin']} slots, "
           f"{L['minb']} CTAs of {L['bk']} per SM" if plan is not None else "// ptxas register allocation")
     src = [
@@ -1207,7 +1261,7 @@ def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True):
         src.insert(-1, f"  __device__ __forceinline__ static const short* omap() {{ return rbd_om_{nm}; }}")
         src.insert(-1, "  __device__ __forceinline__ static const unsigned short* oelem() { return "
                    + (f"rbd_oe_{nm}" if not L["ofull"] else "nullptr") + "; }")
-    base = L["nin"] * em.np
+    base = em.in_total
     for k, slot in enumerate(sc):
         src.append(f"    {{ T s, c; rbd_sincos(my[{slot}], &s, &c); my[{base + 2 * k}] = s; my[{base + 2 * k + 1}] = c; }}")
     src.append("    const unsigned a_in = (unsigned)__cvta_generic_to_shared(my);")
@@ -1225,10 +1279,10 @@ def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True):
     return "\n".join(src), em.flops, L
 
 
-def _ws_struct(model, alg, dt, warps, name=None, trees=None, zero_fill=True):
+def _ws_struct(model, alg, dt, warps, name=None, trees=None, zero_fill=True, fext=False):
     """Device header of the warp-specialised mapping (see wsched.py)."""
     from . import wsched
-    P = wsched.plan(model, alg, dt, warps, trees, zero_fill)
+    P = wsched.plan(model, alg, dt, warps, trees, zero_fill, fext)
     em, sched = P["em"], P["sched"]
     n, nin = P["n"], P["nin"]
     T = "double" if dt == "f64" else "float"
@@ -1250,6 +1304,7 @@ def _ws_struct(model, alg, dt, warps, name=None, trees=None, zero_fill=True):
         "  static constexpr int MAP = 1;  // warp-specialised: CTA = 32 knots x W warps",
         f"  static constexpr int W = {warps}, NDOF = {n}, NIN = {nin}, NSC = {P['nsc']};",
         f"  static constexpr int LO = {em.lo}, NP = {em.np};  // input dof window [LO, LO + NP)",
+    ] + _input_consts(em.in_layout) + [
         f"  static constexpr int E0 = {ext[0]}, E1 = {ext[1]}, E2 = {ext[2]};",
         f"  static constexpr int SIN = {P['sin']}, NA = {sched.nslots}, SOUT = {P['sout']};",
         f"  static constexpr bool STAGE = {'true' if P['stage'] else 'false'}, "
@@ -1265,7 +1320,7 @@ def _ws_struct(model, alg, dt, warps, name=None, trees=None, zero_fill=True):
         if op[0] == "sincos":
             slot = op[3]
             src.append(f"    if (warp == {k % warps}) {{ T s, c; rbd_sincos(s_in[{slot * 33} + lane], &s, &c); "
-                       f"s_in[{(nin * em.np + 2 * k) * 33} + lane] = s; s_in[{(nin * em.np + 2 * k + 1) * 33} + lane] = c; }}")
+                       f"s_in[{(em.in_total + 2 * k) * 33} + lane] = s; s_in[{(em.in_total + 2 * k + 1) * 33} + lane] = c; }}")
             k += 1
     src.append("    (void)s_in; (void)warp; (void)lane;")
     src.append("  }")
@@ -1279,7 +1334,7 @@ def _ws_struct(model, alg, dt, warps, name=None, trees=None, zero_fill=True):
         for w, tasks in enumerate(phase):
             if not tasks:
                 continue
-            body = wsched.ptx_block(sched, tasks, dt, nin * em.np, nin * em.np, ar_space, out_space,
+            body = wsched.ptx_block(sched, tasks, dt, em.in_total, em.in_total, ar_space, out_space,
                                     tn["reload_dist"], ctab)
             src.append(f"    case {w}:  // {', '.join(tasks)}")
             src.append('      asm volatile("{\\n\\t"')
@@ -1304,118 +1359,136 @@ def mapping(model, alg, dt):
 
 
 def host_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
-    """TEST-ONLY: plain C++ one-knot programs for the host harness."""
+    """TEST-ONLY: plain C++ one-knot programs for the host harness
+    (Knot_<alg>_<dt>, and Knot_<alg>_<dt>_X with the f_ext input)."""
     files = {}
     for alg in algorithms:
         for dt in dtypes:
-            em = generate_knot(model, alg, dt)
-            L = _layout(model, alg, dt, em, device=False)
-            src = ["#pragma once", '#include "rbd_runtime.cuh"'] + _struct_head(model, alg, dt, L, em.flops) + [
-                "  static inline void run(const T* __restrict__ iq, const T* __restrict__ iqd,",
-                "                         const T* __restrict__ iu, T* __restrict__ o0,",
-                "                         T* __restrict__ o1, T* __restrict__ o2) {",
-                "    (void)iqd; (void)iu; (void)o1; (void)o2;",
-            ] + ["    " + ln for ln in cpp_body(em, L["n"])] + ["  }", "};", ""]
-            files[f"host_{alg}_{dt}.h"] = "\n".join(src)
+            for fx in ((False, True) if alg in FEXT_ALGORITHMS else (False,)):
+                em = generate_knot(model, alg, dt, fext=fx)
+                L = _layout(model, alg, dt, em, device=False)
+                name = f"Knot_{alg}_{dt}" + ("_X" if fx else "")
+                src = ["#pragma once", '#include "rbd_runtime.cuh"'] + _struct_head(model, alg, dt, L, em.flops, name) + [
+                    "  static inline void run(const T* __restrict__ iq, const T* __restrict__ iqd,",
+                    "                         const T* __restrict__ iu, const T* __restrict__ ifx,",
+                    "                         T* __restrict__ o0, T* __restrict__ o1, T* __restrict__ o2) {",
+                    "    (void)iqd; (void)iu; (void)ifx; (void)o1; (void)o2;",
+                ] + ["    " + ln for ln in cpp_body(em, L["n"])] + ["  }", "};", ""]
+                files[f"host_{alg}_{dt}{'_X' if fx else ''}.h"] = "\n".join(src)
     files["host_all.h"] = "\n".join(["#pragma once"] + [f'#include "{f}"' for f in sorted(files)]) + "\n"
     return files
+
+
+def _launch_unit(alg, dt, tag, K, text):
+    """Translation unit of one kernel: its struct + the internal launcher."""
+    return "\n".join([
+        text.replace("#pragma once\n", ""),
+        f'extern "C" int rbd__launch_{alg}_{dt}_{tag}(const void* q, const void* qd, const void* u, const void* fx,',
+        "                                void* o0, void* o1, void* o2, int64_t N, void* stream) {",
+        f"  return rbd_launch_kernel<{K}>(q, qd, u, fx, o0, o1, o2, N, stream);",
+        "}",
+        "",
+    ])
 
 
 def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
     """{file name: text} of the per-robot library plus {(alg, dtype): flops}.
 
-    knots_<alg>_<dt>.h  the one-knot program (plain C++, also host-compilable)
-    k_<alg>_<dt>.cu     its batch kernel + the typed C-ABI entry rbd_<alg>_<dt>
-    main.cu             dispatch table, rbd_get_info, rbd_launch, host sessions
+    k_<alg>_<dt>_<tag>.cu  one kernel (struct with the one-knot program + its
+                           launcher); tag T = thread per knot, W = warp-
+                           specialised, P<k> = part k (root-tree subset), with
+                           an X suffix for the f_ext variant
+    main.cu                dispatch (batch size -> mapping), typed C-ABI
+                           entries rbd_<alg>_<dt>[_fext], rbd_get_info,
+                           rbd_launch[_fext], host sessions
     Separate translation units let nvcc/ptxas run in parallel.
     """
     n = model.n_dof
     fp = model_hash(model)
     files, flops, table = {}, {}, {}
     dispatch = []
+    sig = "(const void*, const void*, const void*, const void*, void*, void*, void*, int64_t, void*);"
+    args = "(q, qd, u, fx, o0, o1, o2, N, stream)"
     for alg in algorithms:
         for dt in dtypes:
             T = "double" if dt == "f64" else "float"
             tn = tuning(model, alg, dt)
             maps = list(tn["maps"])
-            for mp in maps:
-                tag = "W" if mp == "ws" else "T"
-                K = f"Knot_{alg}_{dt}_{tag}"
-                if mp == "ws":
-                    text, fl, L = _ws_struct(model, alg, dt, int(tn["warps"]), K)
+            for fx in ((False, True) if alg in FEXT_ALGORITHMS else (False,)):
+                X = "X" if fx else ""
+                tags = []
+                for mp in maps:
+                    tag = ("W" if mp == "ws" else "T") + X
+                    K = f"Knot_{alg}_{dt}_{tag}"
+                    if mp == "ws":
+                        text, fl, L = _ws_struct(model, alg, dt, int(tn["warps"]), K, fext=fx)
+                    else:
+                        text, fl, L = _knot_struct(model, alg, dt, K, fext=fx)
+                    if not fx:
+                        flops[(alg, dt)] = fl
+                    table[(alg, dt, fx)] = (L["nin"], L["ext"], 8 if dt == "f64" else 4)
+                    files[f"k_{alg}_{dt}_{tag}.cu"] = _launch_unit(alg, dt, tag, K, text)
+                    tags.append(tag)
+                # large batches of a robot with several root trees: one kernel per
+                # part (a group of trees), each mapped on its own (thread per knot
+                # when its register plan fits, else warp-specialised); cross-part
+                # structural zeros by a coalesced memset ("zero_memset") or by part 0
+                parts = tn.get("parts") or []
+                zf = not tn.get("zero_memset")
+                ptags = []
+                for pi, trees in enumerate(parts):
+                    tag = f"P{pi}{X}"
+                    K = f"Knot_{alg}_{dt}_{tag}"
+                    try:
+                        text, fl, L = _knot_struct(model, alg, dt, K, trees=tuple(trees), zero_fill=zf and pi == 0,
+                                                   fext=fx)
+                    except GenerationError:
+                        text, fl, L = _ws_struct(model, alg, dt, int(tn["warps"]), K, trees=tuple(trees),
+                                                 zero_fill=zf and pi == 0, fext=fx)
+                    files[f"k_{alg}_{dt}_{tag}.cu"] = _launch_unit(alg, dt, tag, K, text)
+                    ptags.append(tag)
+                for tag in tags + ptags:
+                    dispatch.append(f'extern "C" int rbd__launch_{alg}_{dt}_{tag}{sig}')
+                if ptags:
+                    seq = " ".join(f"if ((rc = rbd__launch_{alg}_{dt}_{t}{args}) != 0) return rc;" for t in ptags)
+                    zs = ""
+                    if not zf and alg in ("Minv", "gradID", "gradFD"):
+                        es = 8 if dt == "f64" else 4
+                        zs = (f"if ((rc = (int)cudaMemsetAsync(o0, 0, (size_t)N * {n * n * es}, "
+                              f"(cudaStream_t)stream)) != 0) return rc; ")
+                        if alg != "Minv":
+                            zs += (f"if ((rc = (int)cudaMemsetAsync(o1, 0, (size_t)N * {n * n * es}, "
+                                   f"(cudaStream_t)stream)) != 0) return rc; ")
+                    big = f"[&]() {{ int rc; {zs}{seq} return 0; }}()"
                 else:
-                    text, fl, L = _knot_struct(model, alg, dt, K)
-                flops[(alg, dt)] = fl
-                table[(alg, dt)] = (L["nin"], L["ext"], 8 if dt == "f64" else 4)
-                files[f"knots_{alg}_{dt}_{tag}.h"] = text
-                files[f"k_{alg}_{dt}_{tag}.cu"] = "\n".join([
-                    f'#include "knots_{alg}_{dt}_{tag}.h"',
-                    f'extern "C" int rbd__launch_{alg}_{dt}_{tag}(const void* q, const void* qd, const void* u,',
+                    big = f"rbd__launch_{alg}_{dt}_{'T' if 'thread' in maps else 'W'}{X}{args}"
+                if "ws" in maps and (ptags or "thread" in maps):
+                    pick = f"N <= {int(tn['ws_max_n'])} ? rbd__launch_{alg}_{dt}_W{X}{args} : {big}"
+                elif ptags:
+                    pick = big
+                else:
+                    pick = f"rbd__launch_{alg}_{dt}_{'W' if maps[0] == 'ws' else 'T'}{X}{args}"
+                dispatch += [
+                    f'extern "C" int rbd__launch_{alg}_{dt}{"_fext" if fx else ""}(const void* q, const void* qd, '
+                    "const void* u, const void* fx,",
                     "                                void* o0, void* o1, void* o2, int64_t N, void* stream) {",
-                    f"  return rbd_launch_kernel<{K}>(q, qd, u, o0, o1, o2, N, stream);",
+                    f"  return {pick};",
                     "}",
-                    "",
-                ])
-            # large batches of a robot with several root trees: one kernel per
-            # part (a group of trees), each mapped on its own (thread per knot
-            # when its register plan fits, else warp-specialised); the first
-            # part also writes the cross-part structural zeros
-            parts = tn.get("parts") or []
-            # cross-part structural zeros: a coalesced memset of the n x n
-            # outputs before the parts ("memset"), or stores in part 0
-            zf = not tn.get("zero_memset")
-            ptags = []
-            for pi, trees in enumerate(parts):
-                tag = f"P{pi}"
-                K = f"Knot_{alg}_{dt}_{tag}"
-                try:
-                    text, fl, L = _knot_struct(model, alg, dt, K, trees=tuple(trees), zero_fill=zf and pi == 0)
-                except GenerationError:
-                    text, fl, L = _ws_struct(model, alg, dt, int(tn["warps"]), K, trees=tuple(trees),
-                                             zero_fill=zf and pi == 0)
-                files[f"knots_{alg}_{dt}_{tag}.h"] = text
-                files[f"k_{alg}_{dt}_{tag}.cu"] = "\n".join([
-                    f'#include "knots_{alg}_{dt}_{tag}.h"',
-                    f'extern "C" int rbd__launch_{alg}_{dt}_{tag}(const void* q, const void* qd, const void* u,',
-                    "                                void* o0, void* o1, void* o2, int64_t N, void* stream) {",
-                    f"  return rbd_launch_kernel<{K}>(q, qd, u, o0, o1, o2, N, stream);",
-                    "}",
-                    "",
-                ])
-                ptags.append(tag)
-            sig = "(const void*, const void*, const void*, void*, void*, void*, int64_t, void*);"
-            for mp in maps:
-                dispatch.append(f'extern "C" int rbd__launch_{alg}_{dt}_{"W" if mp == "ws" else "T"}{sig}')
-            for tag in ptags:
-                dispatch.append(f'extern "C" int rbd__launch_{alg}_{dt}_{tag}{sig}')
-            args = "(q, qd, u, o0, o1, o2, N, stream)"
-            if ptags:
-                seq = " ".join(f"if ((rc = rbd__launch_{alg}_{dt}_{t}{args}) != 0) return rc;" for t in ptags)
-                zs = ""
-                if not zf and alg in ("Minv", "gradID", "gradFD"):
-                    es = 8 if dt == "f64" else 4
-                    zs = f"if ((rc = (int)cudaMemsetAsync(o0, 0, (size_t)N * {n * n * es}, (cudaStream_t)stream)) != 0) return rc; "
-                    if alg != "Minv":
-                        zs += f"if ((rc = (int)cudaMemsetAsync(o1, 0, (size_t)N * {n * n * es}, (cudaStream_t)stream)) != 0) return rc; "
-                big = f"[&]() {{ int rc; {zs}{seq} return 0; }}()"
-            else:
-                big = f"rbd__launch_{alg}_{dt}_{'T' if 'thread' in maps else 'W'}{args}"
-            if "ws" in maps and (ptags or "thread" in maps):
-                pick = f"N <= {int(tn['ws_max_n'])} ? rbd__launch_{alg}_{dt}_W{args} : {big}"
-            elif ptags:
-                pick = big
-            else:
-                pick = f"rbd__launch_{alg}_{dt}_{'W' if maps[0] == 'ws' else 'T'}{args}"
+                ]
             dispatch += [
-                f'extern "C" int rbd__launch_{alg}_{dt}(const void* q, const void* qd, const void* u,',
-                "                                void* o0, void* o1, void* o2, int64_t N, void* stream) {",
-                f"  return {pick};",
-                "}",
                 f'extern "C" int rbd_{alg}_{dt}(const {T}* q, const {T}* qd, const {T}* u, {T}* o0,',
                 f"                         {T}* o1, {T}* o2, int64_t N, void* stream) {{",
-                f"  return rbd__launch_{alg}_{dt}(q, qd, u, o0, o1, o2, N, stream);",
+                f"  return rbd__launch_{alg}_{dt}(q, qd, u, nullptr, o0, o1, o2, N, stream);",
                 "}",
             ]
+            if alg in FEXT_ALGORITHMS:
+                dispatch += [
+                    f'extern "C" int rbd_{alg}_{dt}_fext(const {T}* q, const {T}* qd, const {T}* u, '
+                    f"const {T}* f_ext, {T}* o0,",
+                    f"                         {T}* o1, {T}* o2, int64_t N, void* stream) {{",
+                    f"  return rbd__launch_{alg}_{dt}_fext(q, qd, u, f_ext, o0, o1, o2, N, stream);",
+                    "}",
+                ]
     main = [
         f"// GENERATED by paper_2109_06976_b200.codegen -- robot {model.name!r}, n_dof={n}",
         f"// model fingerprint sha256 {fp}",
@@ -1427,22 +1500,26 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
     main += [
         "",
         "static int rbd_ndof() { return %d; }" % n,
-        "static const rbd_entry* rbd_entry_for(int alg, int dtype) {",
-        "  static const rbd_entry table[5][2] = {",
+        "static const rbd_entry* rbd_entry_for(int alg, int dtype, int fext) {",
+        "  static const rbd_entry table[5][2][2] = {",
     ]
     for alg in ALGORITHMS:
         row = []
         for dt in DTYPES:
-            if (alg, dt) in table:
-                nin, ext, es = table[(alg, dt)]
-                row.append(f"{{&rbd__launch_{alg}_{dt}, {nin}, {ext[0]}, {ext[1]}, {ext[2]}, {es}}}")
-            else:
-                row.append("{nullptr, 0, 0, 0, 0, 0}")
+            pair = []
+            for fx in (False, True):
+                if (alg, dt, fx) in table:
+                    nin, ext, es = table[(alg, dt, fx)]
+                    fn = f"rbd__launch_{alg}_{dt}{'_fext' if fx else ''}"
+                    pair.append(f"{{&{fn}, {nin}, {ext[0]}, {ext[1]}, {ext[2]}, {es}}}")
+                else:
+                    pair.append("{nullptr, 0, 0, 0, 0, 0}")
+            row.append("{" + ", ".join(pair) + "}")
         main.append("    {" + ", ".join(row) + "},")
     main += [
         "  };",
-        "  if (alg < 0 || alg > 4 || dtype < 0 || dtype > 1) return nullptr;",
-        "  return table[alg][dtype].fn ? &table[alg][dtype] : nullptr;",
+        "  if (alg < 0 || alg > 4 || dtype < 0 || dtype > 1 || fext < 0 || fext > 1) return nullptr;",
+        "  return table[alg][dtype][fext].fn ? &table[alg][dtype][fext] : nullptr;",
         "}",
         "",
         'extern "C" int rbd_get_info(rbd_info* out) {',

@@ -28,8 +28,10 @@
 
 #if defined(__CUDACC__)
 #define RBD_HD __device__ __forceinline__
+#define RBD_HDC __host__ __device__
 #else
 #define RBD_HD inline
+#define RBD_HDC
 #endif
 
 RBD_HD void rbd_sincos(double x, double* s, double* c) {
@@ -77,8 +79,9 @@ __host__ __device__ constexpr bool rbd_ofull() { return rbd_park_traits<K>::oful
 template <class K>
 __global__ void __launch_bounds__(K::BK, K::MINB)
 rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __restrict__ qd,
-                 const typename K::T* __restrict__ u, typename K::T* __restrict__ o0,
-                 typename K::T* __restrict__ o1, typename K::T* __restrict__ o2, long long N) {
+                 const typename K::T* __restrict__ u, const typename K::T* __restrict__ fx,
+                 typename K::T* __restrict__ o0, typename K::T* __restrict__ o1,
+                 typename K::T* __restrict__ o2, long long N) {
   typedef typename K::T T;
   constexpr int BK = K::BK, n = K::NDOF;
   extern __shared__ __align__(16) unsigned char rbd_smem[];
@@ -89,28 +92,29 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
   const int nk = left < BK ? (int)left : BK;
   const int tid = threadIdx.x;
 
-  // all NIN * NP loads of this thread are issued before the first smem store
-  // (one HBM round trip per CTA, not one per element); a part program reads
-  // only its dof window [LO, LO + NP) of each knot's inputs
-  constexpr int NP = K::NP;
-  T v[K::NIN][NP];
+  // all input loads of this thread are issued before the first smem store
+  // (one HBM round trip per CTA, not one per element); input a contributes
+  // its window of inw(a) scalars per knot (a part program's dof window; 6 per
+  // dof for f_ext), at offset ing(a) of the knot's global row of ins(a)
+  constexpr int NT = K::inr(K::NIN - 1) + K::inw(K::NIN - 1);
+  T v[NT];
 #pragma unroll
   for (int a = 0; a < K::NIN; ++a) {
-    const T* src = (a == 0 ? q : (a == 1 ? qd : u)) + base * n + K::LO;
+    const T* src = (a == 0 ? q : (a == 1 ? qd : (a == 2 ? u : fx))) + base * K::ins(a) + K::ing(a);
 #pragma unroll
-    for (int r = 0; r < NP; ++r) {
+    for (int r = 0; r < K::inw(a); ++r) {
       const int idx = tid + r * BK;
-      const int k = idx / NP, j = idx - k * NP;
-      v[a][r] = (idx < nk * NP) ? __ldg(src + k * n + j) : T(0);
+      const int k = idx / K::inw(a), j = idx - k * K::inw(a);
+      v[K::inr(a) + r] = (idx < nk * K::inw(a)) ? __ldg(src + k * K::ins(a) + j) : T(0);
     }
   }
 #pragma unroll
   for (int a = 0; a < K::NIN; ++a) {
 #pragma unroll
-    for (int r = 0; r < NP; ++r) {
+    for (int r = 0; r < K::inw(a); ++r) {
       const int idx = tid + r * BK;
-      const int k = idx / NP, j = idx - k * NP;
-      s_in[k * K::SIN + a * NP + j] = v[a][r];
+      const int k = idx / K::inw(a), j = idx - k * K::inw(a);
+      s_in[k * K::SIN + K::inr(a) + j] = v[K::inr(a) + r];
     }
   }
   short* s_map = reinterpret_cast<short*>(s_in + BK * K::SIN);  // PARK: output list -> row slot
@@ -201,9 +205,9 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
 template <class K>
 __global__ void __launch_bounds__(K::W * 32, K::MINB)
 rbd_ws_kernel(const typename K::T* __restrict__ q, const typename K::T* __restrict__ qd,
-              const typename K::T* __restrict__ u, typename K::T* __restrict__ o0,
-              typename K::T* __restrict__ o1, typename K::T* __restrict__ o2, long long N,
-              typename K::T* __restrict__ garena) {
+              const typename K::T* __restrict__ u, const typename K::T* __restrict__ fx,
+              typename K::T* __restrict__ o0, typename K::T* __restrict__ o1,
+              typename K::T* __restrict__ o2, long long N, typename K::T* __restrict__ garena) {
   typedef typename K::T T;
   constexpr int n = K::NDOF, NT = K::W * 32, L = RBD_WS_LANES;
   extern __shared__ __align__(16) unsigned char rbd_smem[];
@@ -215,26 +219,28 @@ rbd_ws_kernel(const typename K::T* __restrict__ q, const typename K::T* __restri
   for (long long g = blockIdx.x; g < groups; g += gridDim.x) {
     const long long base = g * 32;
     const int nk = (N - base) < 32 ? (int)(N - base) : 32;
-    constexpr int NP = K::NP, PER = (32 * NP + NT - 1) / NT;  // loads per thread per input
-    T v[K::NIN][PER];
+    // input a: 32 knots x inw(a) scalars, PER(a) loads per thread, all in flight
+    constexpr int WMAX = 6 * K::NP;
+    constexpr int PMAX = (32 * WMAX + NT - 1) / NT;
+    T v[K::NIN][PMAX];
 #pragma unroll
     for (int a = 0; a < K::NIN; ++a) {
-      const T* src = (a == 0 ? q : (a == 1 ? qd : u)) + base * n + K::LO;
+      const T* src = (a == 0 ? q : (a == 1 ? qd : (a == 2 ? u : fx))) + base * K::ins(a) + K::ing(a);
 #pragma unroll
-      for (int r = 0; r < PER; ++r) {
+      for (int r = 0; r < (32 * K::inw(a) + NT - 1) / NT; ++r) {
         const int idx = tid + r * NT;
-        const int k = idx / NP, j = idx - k * NP;
-        v[a][r] = (idx < nk * NP) ? __ldg(src + k * n + j) : T(0);
+        const int k = idx / K::inw(a), j = idx - k * K::inw(a);
+        v[a][r] = (idx < nk * K::inw(a)) ? __ldg(src + k * K::ins(a) + j) : T(0);
       }
     }
 #pragma unroll
     for (int a = 0; a < K::NIN; ++a) {
 #pragma unroll
-      for (int r = 0; r < PER; ++r) {
+      for (int r = 0; r < (32 * K::inw(a) + NT - 1) / NT; ++r) {
         const int idx = tid + r * NT;
-        if (idx < 32 * NP) {
-          const int k = idx / NP, j = idx - k * NP;
-          s_in[(a * NP + j) * L + k] = v[a][r];
+        if (idx < 32 * K::inw(a)) {
+          const int k = idx / K::inw(a), j = idx - k * K::inw(a);
+          s_in[(K::inr(a) + j) * L + k] = v[a][r];
         }
       }
     }
@@ -304,12 +310,13 @@ struct rbd_dev_cache {
 };
 
 template <class K>
-static int rbd_launch_kernel(const void* q, const void* qd, const void* u, void* o0, void* o1,
-                             void* o2, int64_t N, void* stream) {
+static int rbd_launch_kernel(const void* q, const void* qd, const void* u, const void* fx, void* o0,
+                             void* o1, void* o2, int64_t N, void* stream) {
   typedef typename K::T T;
   if (N < 0) return RBD_EINVAL;
   if (N == 0) return 0;
-  if (!q || (K::NIN == 3 && (!qd || !u)) || !o0 || (K::E1 > 0 && !o1) || (K::E2 > 0 && !o2))
+  if (!q || (K::NIN >= 3 && (!qd || !u)) || (K::NIN == 4 && !fx) || !o0 || (K::E1 > 0 && !o1) ||
+      (K::E2 > 0 && !o2))
     return RBD_EINVAL;
   constexpr size_t smem = rbd_smem_bytes<K>();
   if (smem > 48 * 1024) {
@@ -348,11 +355,12 @@ static int rbd_launch_kernel(const void* q, const void* qd, const void* u, void*
     const long long groups = (N + 31) / 32;
     const long long grid = groups < c.grid ? groups : c.grid;
     rbd_ws_kernel<K><<<(unsigned)grid, K::W * 32, smem, (cudaStream_t)stream>>>(
-        (const T*)q, (const T*)qd, (const T*)u, (T*)o0, (T*)o1, (T*)o2, (long long)N, (T*)c.arena);
+        (const T*)q, (const T*)qd, (const T*)u, (const T*)fx, (T*)o0, (T*)o1, (T*)o2, (long long)N,
+        (T*)c.arena);
   } else {
     const long long grid = (N + K::BK - 1) / K::BK;
     rbd_batch_kernel<K><<<(unsigned)grid, K::BK, smem, (cudaStream_t)stream>>>(
-        (const T*)q, (const T*)qd, (const T*)u, (T*)o0, (T*)o1, (T*)o2, (long long)N);
+        (const T*)q, (const T*)qd, (const T*)u, (const T*)fx, (T*)o0, (T*)o1, (T*)o2, (long long)N);
   }
   return (int)cudaGetLastError();
 }
@@ -360,8 +368,8 @@ static int rbd_launch_kernel(const void* q, const void* qd, const void* u, void*
 // ---------------------------------------------------------------------------
 // dispatch table (filled by the generated file through rbd_entry_for)
 // ---------------------------------------------------------------------------
-typedef int (*rbd_launch_fn)(const void*, const void*, const void*, void*, void*, void*, int64_t,
-                             void*);
+typedef int (*rbd_launch_fn)(const void*, const void*, const void*, const void*, void*, void*, void*,
+                             int64_t, void*);
 struct rbd_entry {
   rbd_launch_fn fn;
   int32_t n_inputs;
@@ -369,18 +377,26 @@ struct rbd_entry {
   int32_t elem;  // sizeof(T)
 };
 #if defined(RBD_MAIN_TU)
-static const rbd_entry* rbd_entry_for(int alg, int dtype);  // defined by the generated main TU
-static int rbd_ndof();                                       // defined by the generated main TU
+static const rbd_entry* rbd_entry_for(int alg, int dtype, int fext);  // generated main TU
+static int rbd_ndof();                                                 // generated main TU
 
 extern "C" int rbd_launch(int alg, int dtype, const void* q, const void* qd, const void* u,
                           void* out0, void* out1, void* out2, int64_t N, void* stream) {
-  const rbd_entry* e = rbd_entry_for(alg, dtype);
+  const rbd_entry* e = rbd_entry_for(alg, dtype, 0);
   if (!e) return RBD_EINVAL;
-  return e->fn(q, qd, u, out0, out1, out2, N, stream);
+  return e->fn(q, qd, u, nullptr, out0, out1, out2, N, stream);
+}
+
+extern "C" int rbd_launch_fext(int alg, int dtype, const void* q, const void* qd, const void* u,
+                               const void* f_ext, void* out0, void* out1, void* out2, int64_t N,
+                               void* stream) {
+  const rbd_entry* e = rbd_entry_for(alg, dtype, 1);
+  if (!e) return RBD_EINVAL;
+  return e->fn(q, qd, u, f_ext, out0, out1, out2, N, stream);
 }
 
 extern "C" int rbd_alg_extents(int alg, int32_t* n_inputs, int64_t* e0, int64_t* e1, int64_t* e2) {
-  const rbd_entry* e = rbd_entry_for(alg, RBD_F64);
+  const rbd_entry* e = rbd_entry_for(alg, RBD_F64, 0);
   if (!e) return RBD_EINVAL;
   if (n_inputs) *n_inputs = e->n_inputs;
   if (e0) *e0 = e->e0;
@@ -429,18 +445,19 @@ extern "C" int rbd_session_create(int device, int64_t chunk_knots, int32_t slots
   cudaGetDevice(&prev);
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return (int)e;
-  // size for the largest per-knot footprint over all algorithms, fp64
+  // size for the largest per-knot footprint over all algorithms, fp64,
+  // f_ext (6 per dof) included
   int64_t per_knot = 0;
   for (int a = 0; a < 5; ++a) {
-    const rbd_entry* en = rbd_entry_for(a, RBD_F64);
-    int64_t f = (int64_t)en->n_inputs * rbd_ndof() + en->e0 + en->e1 + en->e2;
+    const rbd_entry* en = rbd_entry_for(a, RBD_F64, 0);
+    int64_t f = (int64_t)en->n_inputs * rbd_ndof() + 6 * rbd_ndof() + en->e0 + en->e1 + en->e2;
     if (f > per_knot) per_knot = f;
   }
   rbd_session* s = new rbd_session();
   s->device = device;
   s->chunk = chunk_knots;
   s->slots = slots;
-  s->slot_bytes = (size_t)per_knot * (size_t)chunk_knots * sizeof(double) + 8 * 256;
+  s->slot_bytes = (size_t)per_knot * (size_t)chunk_knots * sizeof(double) + 10 * 256;
   e = cudaHostAlloc((void**)&s->hstage, RBD_ZC_BYTES, cudaHostAllocMapped | cudaHostAllocPortable);
   if (e != cudaSuccess) {
     delete s;
@@ -482,15 +499,17 @@ extern "C" int rbd_session_destroy(rbd_session* s) {
   return 0;
 }
 
-extern "C" int rbd_run_host(rbd_session* s, int alg, int dtype, const void* q, const void* qd,
-                            const void* u, void* out0, void* out1, void* out2, int64_t N) {
+static int rbd_run_host_impl(rbd_session* s, int alg, int dtype, const void* q, const void* qd,
+                             const void* u, const void* fx, void* out0, void* out1, void* out2,
+                             int64_t N) {
   if (!s) return RBD_ESESSION;
-  const rbd_entry* e = rbd_entry_for(alg, dtype);
+  const rbd_entry* e = rbd_entry_for(alg, dtype, fx ? 1 : 0);
   if (!e || N < 0) return RBD_EINVAL;
   if (N == 0) return 0;
   const int64_t n = rbd_ndof();
   const size_t es = (size_t)e->elem;
-  const void* hin[3] = {q, qd, u};
+  const void* hin[4] = {q, qd, u, fx};
+  const int64_t iext[4] = {n, n, n, 6 * n};  // per-knot input extents (f_ext: 6 per dof)
   void* hout[3] = {out0, out1, out2};
   const int64_t ext[3] = {e->e0, e->e1, e->e2};
   for (int a = 0; a < e->n_inputs; ++a)
@@ -502,11 +521,12 @@ extern "C" int rbd_run_host(rbd_session* s, int alg, int dtype, const void* q, c
   cudaError_t err = cudaSetDevice(s->device);
   if (err != cudaSuccess) return (int)err;
   int rc = 0;
-  size_t in_bytes = (size_t)(e->n_inputs * N * n) * es, out_bytes = 0;
+  size_t in_bytes = 0, out_bytes = 0;
+  for (int a = 0; a < e->n_inputs; ++a) in_bytes += (size_t)(N * iext[a]) * es;
   for (int b = 0; b < 3; ++b) out_bytes += (size_t)(N * ext[b]) * es;
   if (in_bytes + out_bytes + 8 * 256 <= RBD_ZC_BYTES) {
     // zero-copy: device pointers of pinned caller buffers, else the pinned stage
-    const void* din[3] = {nullptr, nullptr, nullptr};
+    const void* din[4] = {nullptr, nullptr, nullptr, nullptr};
     void* dout[3] = {nullptr, nullptr, nullptr};
     bool direct = true;
     for (int a = 0; a < e->n_inputs && direct; ++a) direct = (din[a] = rbd_mapped(hin[a])) != nullptr;
@@ -515,7 +535,7 @@ extern "C" int rbd_run_host(rbd_session* s, int alg, int dtype, const void* q, c
     unsigned char* hp = s->hstage;
     if (!direct) {
       for (int a = 0; a < e->n_inputs; ++a) {
-        const size_t bytes = (size_t)(N * n) * es;
+        const size_t bytes = (size_t)(N * iext[a]) * es;
         memcpy(hp, hin[a], bytes);
         din[a] = rbd_mapped(hp);
         hp += rbd_align256(bytes);
@@ -527,11 +547,11 @@ extern "C" int rbd_run_host(rbd_session* s, int alg, int dtype, const void* q, c
       }
     }
     cudaStream_t st = s->stream[0];
-    rc = e->fn(din[0], din[1], din[2], dout[0], dout[1], dout[2], N, (void*)st);
+    rc = e->fn(din[0], din[1], din[2], din[3], dout[0], dout[1], dout[2], N, (void*)st);
     if (rc == 0) rc = (int)cudaStreamSynchronize(st);
     if (rc == 0 && !direct) {
       hp = s->hstage;
-      for (int a = 0; a < e->n_inputs; ++a) hp += rbd_align256((size_t)(N * n) * es);
+      for (int a = 0; a < e->n_inputs; ++a) hp += rbd_align256((size_t)(N * iext[a]) * es);
       for (int b = 0; b < 3; ++b) {
         if (!ext[b]) continue;
         const size_t bytes = (size_t)(N * ext[b]) * es;
@@ -547,11 +567,11 @@ extern "C" int rbd_run_host(rbd_session* s, int alg, int dtype, const void* q, c
     const int64_t nk = (N - k0) < s->chunk ? (N - k0) : s->chunk;
     cudaStream_t st = s->stream[slot];
     unsigned char* p = s->dbuf[slot];
-    const void* din[3] = {nullptr, nullptr, nullptr};
+    const void* din[4] = {nullptr, nullptr, nullptr, nullptr};
     void* dout[3] = {nullptr, nullptr, nullptr};
     for (int a = 0; a < e->n_inputs; ++a) {
-      const size_t bytes = (size_t)(nk * n) * es;
-      err = cudaMemcpyAsync(p, (const unsigned char*)hin[a] + (size_t)(k0 * n) * es, bytes,
+      const size_t bytes = (size_t)(nk * iext[a]) * es;
+      err = cudaMemcpyAsync(p, (const unsigned char*)hin[a] + (size_t)(k0 * iext[a]) * es, bytes,
                             cudaMemcpyHostToDevice, st);
       if (err != cudaSuccess) { rc = (int)err; break; }
       din[a] = p;
@@ -563,7 +583,7 @@ extern "C" int rbd_run_host(rbd_session* s, int alg, int dtype, const void* q, c
       dout[b] = p;
       p += rbd_align256((size_t)(nk * ext[b]) * es);
     }
-    rc = e->fn(din[0], din[1], din[2], dout[0], dout[1], dout[2], nk, (void*)st);
+    rc = e->fn(din[0], din[1], din[2], din[3], dout[0], dout[1], dout[2], nk, (void*)st);
     if (rc) break;
     for (int b = 0; b < 3; ++b) {
       if (ext[b] == 0) continue;
@@ -578,6 +598,18 @@ extern "C" int rbd_run_host(rbd_session* s, int alg, int dtype, const void* q, c
   }
   cudaSetDevice(prev);
   return rc;
+}
+
+extern "C" int rbd_run_host(rbd_session* s, int alg, int dtype, const void* q, const void* qd,
+                            const void* u, void* out0, void* out1, void* out2, int64_t N) {
+  return rbd_run_host_impl(s, alg, dtype, q, qd, u, nullptr, out0, out1, out2, N);
+}
+
+extern "C" int rbd_run_host_fext(rbd_session* s, int alg, int dtype, const void* q, const void* qd,
+                                 const void* u, const void* f_ext, void* out0, void* out1,
+                                 void* out2, int64_t N) {
+  if (!f_ext) return RBD_EINVAL;
+  return rbd_run_host_impl(s, alg, dtype, q, qd, u, f_ext, out0, out1, out2, N);
 }
 
 extern "C" int rbd_bench_host(rbd_session* s, int alg, int dtype, const void* q, const void* qd,

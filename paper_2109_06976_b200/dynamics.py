@@ -22,9 +22,10 @@ or a batch `(N, n)`:
 float32 inputs select the fp32 kernels, everything else fp64 (the reference
 precision); `dtype="f32"|"f64"` overrides.  Shapes other than (n,) / (N, n)
 raise ValueError as `refdyn._check_state` does (`refdyn.py:31-38`); host
-inputs containing non-finite values raise ValueError too.  `f_ext` is not an
-input of the generated kernels (nor of the reference's generated programs,
-`codegen.py` has none) and raises NotImplementedError when given.
+inputs containing non-finite values raise ValueError too.  `f_ext` (per-link
+external forces in link coordinates, refdyn.py:79-80) is `(n, 6)` for one
+knot or `(N, n, 6)`, and runs the f_ext kernels (`rbd_<alg>_<dt>_fext`; the
+reference's generated programs have no f_ext input, its refdyn does).
 """
 
 from dataclasses import dataclass
@@ -80,8 +81,17 @@ def _shape_check(model, arrs):
     return single, N
 
 
-def _run(model, alg, args, dtype=None, device=None):
-    """Evaluate `alg` on state arguments `args` (1 or 3 arrays)."""
+def _fext_shape(model, fx, single, N):
+    n = model.n_dof
+    shp = tuple(fx.shape)
+    want = (n, 6) if single else (N, n, 6)
+    if shp != want:
+        raise ValueError(f"f_ext has shape {shp}, expected {want}")
+
+
+def _run(model, alg, args, dtype=None, device=None, f_ext=None):
+    """Evaluate `alg` on state arguments `args` (1 or 3 arrays), optionally
+    with per-link external forces f_ext."""
     dt = _resolve_dtype(args, dtype)
     on_device = _is_torch(args[0]) and args[0].is_cuda
     lib = runtime.robot_library(model)
@@ -96,11 +106,18 @@ def _run(model, alg, args, dtype=None, device=None):
                 raise ValueError("mixing device and host state arguments")
             xs.append(x.to(tdt).contiguous())
         single, N = _shape_check(model, xs)
+        fx = None
+        if f_ext is not None:
+            if not (_is_torch(f_ext) and f_ext.is_cuda and f_ext.device == dev):
+                raise ValueError("mixing device and host state arguments")
+            fx = f_ext.to(tdt).contiguous()
+            _fext_shape(model, fx, single, N)
         outs = [torch.empty((N, e), dtype=tdt, device=dev) for _, e in codegen.outputs(alg, n)]
         with torch.cuda.device(dev):
             stream = torch.cuda.current_stream(dev).cuda_stream
             runtime.launch(lib, alg, dt, [x.data_ptr() for x in xs],
-                           [o.data_ptr() for o in outs], N, stream)
+                           [o.data_ptr() for o in outs], N, stream,
+                           fext_ptr=None if fx is None else fx.data_ptr())
     else:
         ndt = np.float32 if dt == "f32" else np.float64
         xs = []
@@ -109,11 +126,19 @@ def _run(model, alg, args, dtype=None, device=None):
                 x = x.detach().cpu().numpy()
             xs.append(np.ascontiguousarray(np.asarray(x, dtype=ndt)))
         single, N = _shape_check(model, xs)
-        for x in xs:
+        fx = None
+        if f_ext is not None:
+            fx = f_ext.detach().cpu().numpy() if _is_torch(f_ext) else f_ext
+            fx = np.ascontiguousarray(np.asarray(fx, dtype=ndt))
+            _fext_shape(model, fx, single, N)
+            xs_check = xs + [fx]
+        else:
+            xs_check = xs
+        for x in xs_check:
             if not np.all(np.isfinite(x)):
                 raise ValueError("state vector contains non-finite entries")
         outs = [np.empty((N, e), dtype=ndt) for _, e in codegen.outputs(alg, n)]
-        runtime.run_host(lib, alg, dt, xs, outs, N, device=device)
+        runtime.run_host(lib, alg, dt, xs, outs, N, device=device, f_ext=fx)
     shaped = []
     for (nm, e), o in zip(codegen.outputs(alg, n), outs):
         shp = (n, n) if e == n * n else (n,)
@@ -121,26 +146,19 @@ def _run(model, alg, args, dtype=None, device=None):
     return shaped
 
 
-def _no_fext(f_ext):
-    if f_ext is not None:
-        raise NotImplementedError("f_ext is not an input of the generated kernels")
-
-
 def rnea(model, q, qd, qdd, f_ext=None, dtype=None):
     """Inverse dynamics (reference `refdyn.py:91-94`)."""
-    _no_fext(f_ext)
-    return _run(model, "ID", [q, qd, qdd], dtype)[0]
+    return _run(model, "ID", [q, qd, qdd], dtype, f_ext=f_ext)[0]
 
 
 def bias_force(model, q, qd, f_ext=None, dtype=None):
     """rnea at qdd = 0 (reference `refdyn.py:97-100`)."""
-    _no_fext(f_ext)
     if _is_torch(q):
         import torch
         zero = torch.zeros_like(q)
     else:
         zero = np.zeros_like(np.asarray(q, dtype=np.float32 if _resolve_dtype([q], dtype) == "f32" else np.float64))
-    return _run(model, "ID", [q, qd, zero], dtype)[0]
+    return _run(model, "ID", [q, qd, zero], dtype, f_ext=f_ext)[0]
 
 
 def minv_direct(model, q, dtype=None):
@@ -150,20 +168,17 @@ def minv_direct(model, q, dtype=None):
 
 def forward_dynamics(model, q, qd, tau, f_ext=None, dtype=None):
     """qdd = Minv (tau - c) (reference `refdyn.py:172-175`)."""
-    _no_fext(f_ext)
-    return _run(model, "FD", [q, qd, tau], dtype)[0]
+    return _run(model, "FD", [q, qd, tau], dtype, f_ext=f_ext)[0]
 
 
 def rnea_grad(model, q, qd, qdd, f_ext=None, dtype=None):
     """(dtau/dq, dtau/dqd) (reference `refdyn.py:178-239`)."""
-    _no_fext(f_ext)
-    dq, dqd = _run(model, "gradID", [q, qd, qdd], dtype)
+    dq, dqd = _run(model, "gradID", [q, qd, qdd], dtype, f_ext=f_ext)
     return DynamicsGradients(dq, dqd)
 
 
 def fd_grad(model, q, qd, tau, f_ext=None, dtype=None):
     """(dqdd/dq, dqdd/dqd) = -Minv dID at qdd = FD(q, qd, tau)
     (reference `refdyn.py:242-249`); the solved qdd rides along."""
-    _no_fext(f_ext)
-    dq, dqd, qdd = _run(model, "gradFD", [q, qd, tau], dtype)
+    dq, dqd, qdd = _run(model, "gradFD", [q, qd, tau], dtype, f_ext=f_ext)
     return DynamicsGradients(dq, dqd, qdd)

@@ -141,9 +141,10 @@ class RbdInfo(ctypes.Structure):
                 ("robot", ctypes.c_char_p), ("fingerprint", ctypes.c_char_p)]
 
 
-ABI_SYMBOLS = (["rbd_get_info", "rbd_alg_extents", "rbd_launch", "rbd_session_create",
-                "rbd_session_destroy", "rbd_run_host", "rbd_bench_host"]
-               + [f"rbd_{a}_{d}" for a in codegen.ALGORITHMS for d in codegen.DTYPES])
+ABI_SYMBOLS = (["rbd_get_info", "rbd_alg_extents", "rbd_launch", "rbd_launch_fext", "rbd_session_create",
+                "rbd_session_destroy", "rbd_run_host", "rbd_run_host_fext", "rbd_bench_host"]
+               + [f"rbd_{a}_{d}" for a in codegen.ALGORITHMS for d in codegen.DTYPES]
+               + [f"rbd_{a}_{d}_fext" for a in codegen.FEXT_ALGORITHMS for d in codegen.DTYPES])
 
 _vp = ctypes.c_void_p
 
@@ -152,6 +153,8 @@ def _bind(lib):
     lib.rbd_get_info.argtypes = [ctypes.POINTER(RbdInfo)]
     lib.rbd_alg_extents.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int32)] + [ctypes.POINTER(ctypes.c_int64)] * 3
     lib.rbd_launch.argtypes = [ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp]
+    lib.rbd_launch_fext.argtypes = [ctypes.c_int, ctypes.c_int] + [_vp] * 7 + [ctypes.c_int64, _vp]
+    lib.rbd_run_host_fext.argtypes = [_vp, ctypes.c_int, ctypes.c_int] + [_vp] * 7 + [ctypes.c_int64]
     lib.rbd_session_create.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(_vp)]
     lib.rbd_session_destroy.argtypes = [_vp]
     lib.rbd_run_host.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64]
@@ -161,6 +164,8 @@ def _bind(lib):
         for d in codegen.DTYPES:
             fn = getattr(lib, f"rbd_{a}_{d}")
             fn.argtypes = [_vp] * 6 + [ctypes.c_int64, _vp]
+            if a in codegen.FEXT_ALGORITHMS:
+                getattr(lib, f"rbd_{a}_{d}_fext").argtypes = [_vp] * 7 + [ctypes.c_int64, _vp]
     for s in ABI_SYMBOLS:
         getattr(lib, s).restype = ctypes.c_int
     return lib

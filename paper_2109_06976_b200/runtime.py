@@ -41,14 +41,21 @@ def robot_library(model):
     return kernels.library(model)
 
 
-def launch(lib, alg, dtype, in_ptrs, out_ptrs, N, stream):
-    """One batched kernel launch on device pointers (asynchronous)."""
+def launch(lib, alg, dtype, in_ptrs, out_ptrs, N, stream, fext_ptr=None):
+    """One batched kernel launch on device pointers (asynchronous); with
+    fext_ptr, the f_ext entry rbd_<alg>_<dt>_fext."""
     ins = list(in_ptrs) + [None] * (3 - len(in_ptrs))
     outs = list(out_ptrs) + [None] * (3 - len(out_ptrs))
-    fn = getattr(lib, f"rbd_{alg}_{dtype}")
-    rc = fn(*[ctypes.c_void_p(p) if p else None for p in ins + outs], ctypes.c_int64(N),
-            ctypes.c_void_p(stream) if stream else None)
-    check(rc, f"rbd_{alg}_{dtype}")
+    vp = lambda p: ctypes.c_void_p(p) if p else None
+    st = ctypes.c_void_p(stream) if stream else None
+    if fext_ptr is not None:
+        name = f"rbd_{alg}_{dtype}_fext"
+        rc = getattr(lib, name)(*[vp(p) for p in ins], vp(fext_ptr), *[vp(p) for p in outs],
+                                ctypes.c_int64(N), st)
+    else:
+        name = f"rbd_{alg}_{dtype}"
+        rc = getattr(lib, name)(*[vp(p) for p in ins + outs], ctypes.c_int64(N), st)
+    check(rc, name)
 
 
 class Session:
@@ -63,9 +70,14 @@ class Session:
               "rbd_session_create")
         self.handle = h
 
-    def run(self, alg, dtype, in_arrays, out_arrays, N):
+    def run(self, alg, dtype, in_arrays, out_arrays, N, f_ext=None):
         ins = [a.ctypes.data_as(ctypes.c_void_p) for a in in_arrays] + [None] * (3 - len(in_arrays))
         outs = [a.ctypes.data_as(ctypes.c_void_p) for a in out_arrays] + [None] * (3 - len(out_arrays))
+        if f_ext is not None:
+            rc = self.lib.rbd_run_host_fext(self.handle, _ALG_ID[alg], _DT_ID[dtype], *ins,
+                                            f_ext.ctypes.data_as(ctypes.c_void_p), *outs, ctypes.c_int64(N))
+            check(rc, f"rbd_run_host_fext({alg}, {dtype})")
+            return
         rc = self.lib.rbd_run_host(self.handle, _ALG_ID[alg], _DT_ID[dtype], *ins, *outs, ctypes.c_int64(N))
         check(rc, f"rbd_run_host({alg}, {dtype})")
 
@@ -118,5 +130,5 @@ def session(lib, device=0):
         return s
 
 
-def run_host(lib, alg, dtype, in_arrays, out_arrays, N, device=None):
-    session(lib, 0 if device is None else device).run(alg, dtype, in_arrays, out_arrays, N)
+def run_host(lib, alg, dtype, in_arrays, out_arrays, N, device=None, f_ext=None):
+    session(lib, 0 if device is None else device).run(alg, dtype, in_arrays, out_arrays, N, f_ext)

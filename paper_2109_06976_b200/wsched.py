@@ -264,17 +264,17 @@ def ptx_block(sched, tasks, dtype, scratch_base, nin_slots, arena_space, out_spa
     return head + lines
 
 
-def plan(model, alg, dtype, warps, trees=None, zero_fill=True):
+def plan(model, alg, dtype, warps, trees=None, zero_fill=True, fext=False):
     """Schedule + memory plan of the warp-specialised kernel."""
-    em = cg.generate_knot(model, alg, dtype, trees, zero_fill)
+    em = cg.generate_knot(model, alg, dtype, trees, zero_fill, fext=fext)
     sched = Schedule(em, warps)
     n = model.n_dof
     es = 8 if dtype == "f64" else 4
-    nin = len(cg.INPUTS[alg])
+    nin = len(em.in_layout)
     nsc = sum(1 for op in em.ops if op[0] == "sincos")
     ext = [e for _, e in cg.outputs(alg, n)]
     ext += [0] * (3 - len(ext))
-    sin = nin * em.np + 2 * nsc
+    sin = em.in_total + 2 * nsc
     row = LANES * es
     sout = sum(ext)
     opts = [(True, True), (True, False), (False, True), (False, False)]  # (arena smem, stage outputs)

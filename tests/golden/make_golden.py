@@ -9,7 +9,9 @@ numpy only) in the build container and records, for every bundled robot:
   seed 0) and the reference outputs of rnea / minv_direct /
   forward_dynamics / rnea_grad / fd_grad (`refdyn.py:91-249`), in the
   operator's I/O naming (`schedule.py:208-226`);
-* for gradFD also qdd (the kernel's extra output).
+* for gradFD also qdd (the kernel's extra output);
+* the same four f_ext-taking entries with seeded per-link external forces
+  f_ext ~ U(-1, 1), shape (N, n, 6), seed 2 (refdyn.py:79-80), keys "fext.*".
 
 The reference cannot travel to the GPU box, so the fixtures are committed:
 
@@ -66,6 +68,18 @@ def main():
             outs["gradFD.dq_out"].append(g.dq.ravel())
             outs["gradFD.dqd_out"].append(g.dqd.ravel())
             outs["gradFD.qdd_out"].append(refdyn.forward_dynamics(m, q[k], qd[k], u[k]))
+        fx = np.random.default_rng(2).uniform(-1.0, 1.0, size=(N_KNOTS, n, 6))
+        rec["f_ext"] = fx
+        for k in range(N_KNOTS):
+            outs.setdefault("fext.ID.tau_out", []).append(refdyn.rnea(m, q[k], qd[k], u[k], fx[k]))
+            outs.setdefault("fext.FD.qdd_out", []).append(refdyn.forward_dynamics(m, q[k], qd[k], u[k], fx[k]))
+            g = refdyn.rnea_grad(m, q[k], qd[k], u[k], fx[k])
+            outs.setdefault("fext.gradID.dq_out", []).append(g.dq.ravel())
+            outs.setdefault("fext.gradID.dqd_out", []).append(g.dqd.ravel())
+            g = refdyn.fd_grad(m, q[k], qd[k], u[k], fx[k])
+            outs.setdefault("fext.gradFD.dq_out", []).append(g.dq.ravel())
+            outs.setdefault("fext.gradFD.dqd_out", []).append(g.dqd.ravel())
+            outs.setdefault("fext.gradFD.qdd_out", []).append(refdyn.forward_dynamics(m, q[k], qd[k], u[k], fx[k]))
         for key, v in outs.items():
             rec[key] = np.array(v)
         path = os.path.join(HERE, f"{name}.npz")

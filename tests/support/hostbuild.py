@@ -31,16 +31,24 @@ def host_library(model, opt="-O0"):
         os.replace(so + ".tmp", so)
     lib = ctypes.CDLL(so)
     lib.host_eval.argtypes = [ctypes.c_int, ctypes.c_int] + [ctypes.c_void_p] * 6 + [ctypes.c_int64]
+    lib.host_eval_fext.argtypes = [ctypes.c_int, ctypes.c_int] + [ctypes.c_void_p] * 7 + [ctypes.c_int64]
     return lib
 
 
-def host_eval(lib, model, alg, dtype, q, qd, u):
+def host_eval(lib, model, alg, dtype, q, qd, u, f_ext=None):
     ndt = np.float64 if dtype == "f64" else np.float32
     arrs = [np.ascontiguousarray(x, dtype=ndt) for x in (q, qd, u)]
     N = arrs[0].shape[0]
     outs = [np.zeros((N, e), ndt) for _, e in codegen.outputs(alg, model.n_dof)]
     ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    optrs = [ptr(o) for o in outs] + [None] * (3 - len(outs))
+    if f_ext is not None:
+        fx = np.ascontiguousarray(f_ext, dtype=ndt).reshape(N, -1)
+        rc = lib.host_eval_fext(codegen.ALGORITHMS.index(alg), codegen.DTYPES.index(dtype),
+                                *[ptr(a) for a in arrs], ptr(fx), *optrs, N)
+        assert rc == 0
+        return {nm: o for (nm, _), o in zip(codegen.outputs(alg, model.n_dof), outs)}
     rc = lib.host_eval(codegen.ALGORITHMS.index(alg), codegen.DTYPES.index(dtype),
-                       *[ptr(a) for a in arrs], *([ptr(o) for o in outs] + [None] * (3 - len(outs))), N)
+                       *[ptr(a) for a in arrs], *optrs, N)
     assert rc == 0
     return {nm: o for (nm, _), o in zip(codegen.outputs(alg, model.n_dof), outs)}

@@ -49,7 +49,7 @@ def test_generation_is_deterministic_and_folds_constants():
     b, fb = codegen.generate_sources(m)
     assert a == b and fa == fb
     # the model's numbers are literals: no parent tables or inertia arrays in the source
-    src = a["knots_gradFD_f64_T.h"] + a["knots_gradFD_f64_W.h"]
+    src = a["k_gradFD_f64_T.cu"] + a["k_gradFD_f64_W.cu"]
     assert "parent" not in src and "[6][6]" not in src
     # fewer flops than the reference program's IR count for gradFD on chain7 (17,131)
     assert fa[("gradFD", "f64")] < 17131
@@ -66,3 +66,16 @@ def test_seeded_random_states_match_oracle():
         out = hostbuild.host_eval(lib, m, alg, "f64", q, qd, u)
         for nm in ref:
             assert rel_err(out[nm], ref[nm]) < 1e-12
+
+
+@pytest.mark.parametrize("name", ["chain7", "mixed5", "quad12", "tree7"])
+def test_fext_programs_match_reference(name):
+    """f_ext (per-link external forces, refdyn.py:79-80) through the generated
+    programs vs the reference's outputs with seeded forces (golden 'fext.*')."""
+    g = golden(name)
+    m = models.load(name)
+    lib = hostbuild.host_library(m)
+    for alg in codegen.FEXT_ALGORITHMS:
+        out = hostbuild.host_eval(lib, m, alg, "f64", g["q"], g["qd"], g["u"], f_ext=g["f_ext"])
+        for nm, v in out.items():
+            assert rel_err(v, g[f"fext.{alg}.{nm}"]) < TOL["f64"], (name, alg, nm)

@@ -150,8 +150,49 @@ def test_errors_like_reference():
         dynamics.rnea(m, np.zeros(6), np.zeros(7), np.zeros(7))
     with pytest.raises(ValueError):
         dynamics.rnea(m, np.full(7, np.inf), np.zeros(7), np.zeros(7))
-    with pytest.raises(NotImplementedError):
-        dynamics.rnea(m, np.zeros(7), np.zeros(7), np.zeros(7), f_ext=np.zeros((7, 6)))
+    with pytest.raises(ValueError):  # f_ext must be (n, 6) for one knot
+        dynamics.rnea(m, np.zeros(7), np.zeros(7), np.zeros(7), f_ext=np.zeros((7, 5)))
+    with pytest.raises(ValueError):
+        dynamics.rnea(m, np.zeros(7), np.zeros(7), np.zeros(7), f_ext=np.full((7, 6), np.nan))
+
+
+@pytest.mark.parametrize("name", MODELS)
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_fext_matches_reference(name, dt):
+    """The f_ext entries (refdyn's f_ext argument) against the reference's
+    own outputs with seeded external forces, on both kernel mappings (golden
+    knots, and tiled past the small-batch threshold), device and host paths."""
+    g = golden(name)
+    m = models.load(name)
+    n = m.n_dof
+    big = int(codegen.tuning(m, "gradFD", dt)["ws_max_n"]) + 37
+    for N in (g["q"].shape[0], big):
+        reps = -(-N // g["q"].shape[0])
+        tile = lambda x: np.tile(x, (reps,) + (1,) * (x.ndim - 1))[:N]
+        q, qd, u, fx = (tile(g[k]) for k in ("q", "qd", "u", "f_ext"))
+        tdt = torch.float64 if dt == "f64" else torch.float32
+        for alg in codegen.FEXT_ALGORITHMS:
+            if dt == "f64":
+                refs = {nm: tile(g[f"fext.{alg}.{nm}"]) for nm, _ in codegen.outputs(alg, n)}
+            else:
+                r32 = [g[k].astype(np.float32).astype(np.float64) for k in ("q", "qd", "u", "f_ext")]
+                refs = {k: tile(v) for k, v in R.evaluate_batch(m, alg, *r32).items()}
+            xs = _dev(q, qd, u, fx, dt=tdt)
+            fn = {"ID": dynamics.rnea, "FD": dynamics.forward_dynamics, "gradID": dynamics.rnea_grad,
+                  "gradFD": dynamics.fd_grad}[alg]
+            got = fn(m, *xs[:3], f_ext=xs[3])
+            torch.cuda.synchronize()
+            vals = [got] if alg in ("ID", "FD") else ([got.dq, got.dqd] + ([got.qdd] if alg == "gradFD" else []))
+            for (nm, _), v in zip(codegen.outputs(alg, n), vals):
+                v = v.cpu().numpy().reshape(N, -1)
+                assert rel_err(v, refs[nm]) < TOL[dt], (name, alg, dt, N, nm, rel_err(v, refs[nm]))
+        if N == big or dt == "f32":
+            continue
+        # host path (numpy in, numpy out) through rbd_run_host_fext
+        got = dynamics.fd_grad(m, q, qd, u, f_ext=fx)
+        assert rel_err(got.dq.reshape(N, -1), tile(g["fext.gradFD.dq_out"])) < 1e-9
+        one = dynamics.rnea(m, q[0], qd[0], u[0], f_ext=fx[0])
+        assert rel_err(one[None], g["fext.ID.tau_out"][:1]) < 1e-9
 
 
 @pytest.mark.parametrize("name,dt", [("chain7", "f64"), ("chain7", "f32"), ("humanoid30", "f64")])

@@ -72,3 +72,15 @@ def test_check_state_errors():
         R.rnea(m, np.zeros(6), np.zeros(7), np.zeros(7))
     with pytest.raises(ValueError):
         R.rnea(m, np.full(7, np.nan), np.zeros(7), np.zeros(7))
+
+
+@pytest.mark.parametrize("name", ["link1", "pendulum2", "chain7", "quad12", "humanoid30", "tree7", "mixed5"])
+def test_oracle_fext_pinned_to_reference(name):
+    """The oracle's f_ext path vs the reference's own outputs with seeded
+    per-link external forces (tests/golden/make_golden.py, keys 'fext.*')."""
+    g = golden(name)
+    m = models.load(name)
+    for alg in ("ID", "FD", "gradID", "gradFD"):
+        r = R.evaluate_batch(m, alg, g["q"], g["qd"], g["u"], g["f_ext"])
+        for nm, v in r.items():
+            assert rel_err(v, g[f"fext.{alg}.{nm}"]) < 1e-12, (name, alg, nm)

@@ -22,10 +22,10 @@ def _sincos_slots(em):
     return [op[3] for op in em.ops if op[0] == "sincos"]
 
 
-def run_thread(model, alg, dt, x, stage, budget=None, park=False):
-    em = codegen.generate_knot(model, alg, dt)
+def run_thread(model, alg, dt, x, stage, budget=None, park=False, fext=False):
+    em = codegen.generate_knot(model, alg, dt, fext=fext)
     n = model.n_dof
-    nin = len(codegen.INPUTS[alg])
+    nin = em.in_total // n
     ctab = codegen.ConstTable("K", dt)
     plan = None
     if budget:
@@ -49,10 +49,11 @@ def run_thread(model, alg, dt, x, stage, budget=None, park=False):
     return [np.array([o.get(i, np.nan) for i in range(e)]) for o, (_, e) in zip(outs, codegen.outputs(alg, n))]
 
 
-def run_ws(model, alg, dt, x, warps, arena_space="shared", out_space="shared"):
-    P = wsched.plan(model, alg, dt, warps)
+def run_ws(model, alg, dt, x, warps, arena_space="shared", out_space="shared", fext=False):
+    P = wsched.plan(model, alg, dt, warps, fext=fext)
     S = P["sched"]
-    n, nin = P["n"], P["nin"]
+    n = P["n"]
+    nin = P["em"].in_total // n
     es = 8 if dt == "f64" else 4
     L = wsched.LANES
     row = {i: float(v) for i, v in enumerate(x)}
@@ -215,3 +216,21 @@ def test_spill_plan_invariants():
     tight = codegen.SpillPlan(em, 8, homes, 35)
     loose = codegen.SpillPlan(em, 119, homes, 35)
     assert tight.reloads > loose.reloads and loose.stores <= tight.stores
+
+
+@pytest.mark.parametrize("name", ["chain7", "quad12", "mixed5"])
+@pytest.mark.parametrize("mapping", ["thread_park", "ws"])
+def test_device_ptx_with_fext(name, mapping):
+    """The f_ext kernels' PTX (f_ext staged after q, qd, u in the knot's row)
+    against the reference's outputs with seeded external forces."""
+    g = golden(name)
+    m = models.load(name)
+    n = m.n_dof
+    for alg in codegen.FEXT_ALGORITHMS:
+        x = np.concatenate([_inputs(g, alg, 3, n), g["f_ext"][3].ravel()])
+        if mapping == "thread_park":
+            outs = run_thread(m, alg, "f64", x, stage=False, budget=40, park=True, fext=True)
+        else:
+            outs, _ = run_ws(m, alg, "f64", x, warps=5, arena_space="global", out_space="global", fext=True)
+        for (nm, _), o in zip(codegen.outputs(alg, n), outs):
+            assert rel_err(o[None], g[f"fext.{alg}.{nm}"][3:4]) < 1e-12, (name, alg, nm)
