@@ -724,10 +724,14 @@ TUNING_DEFAULT = {
     "reload_dist": 0,    # re-load smem-resident inputs when the last load is > k ops old (0: load once)
     "stage_kb": 64,      # stage outputs in smem when BK * outputs fit in this many KiB
     "ra": True,          # thread: generator register allocation, spills parked in the smem row
-    "warps_per_sm": 8,   # thread + ra: target occupancy (lowered until the row fits)
+    "warps_per_sm": 16,  # thread + ra: target occupancy (lowered until the row fits)
+    "park": True,        # thread + ra: park outputs in the row, coalesced write-back
     "ra_budget": 0,      # thread + ra: cap on values kept in registers (0: from the register cap)
 }
 TUNED = {}
+# measured on B200 (N = 2^20): chain7 gradFD fp64 is compute-bound at 6 warps/SM
+# either way; per-thread output stores beat parking there (1.35 vs 1.43 ms)
+TUNED[("chain7", "gradFD", "f64")] = {"park": False}
 for _a in ALGORITHMS:
     for _d in DTYPES:
         # measured on B200: with outputs parked in the row, quad12's
@@ -1152,15 +1156,18 @@ def _layout(model, alg, dt, em, device=True):
             budget = (regs - REG_OVERHEAD) // (2 if dt == "f64" else 1)
             if tn.get("ra_budget"):
                 budget = min(budget, int(tn["ra_budget"]))
-            row_max = (SM_SMEM - ctas * (CTA_SMEM_RESERVED + 4 * sum(ext) + 16)) // (threads * es)
-            plan = SpillPlan(em, budget, homes, base, park_outputs=True)
+            park = bool(tn.get("park", True))
+            row_max = (SM_SMEM - ctas * (CTA_SMEM_RESERVED + (4 * sum(ext) if park else 0) + 16)) // (threads * es)
+            plan = SpillPlan(em, budget, homes, base, park_outputs=park)
             if _odd(plan.nslots) <= row_max:
                 minb = ctas
                 break
         else:
             raise GenerationError(f"{model.name} {alg} {dt}: no occupancy fits the spill row")
         row = _odd(max(base, plan.nslots))
-        stage = False  # outputs are parked in the row and written back coalesced
+        # parked: outputs parked in the row and written back coalesced; else
+        # each thread stores its outputs to global as they are produced
+        stage = False
         bad = {v for v in plan.outconst.values() if v != 0.0}
         if bad:
             raise GenerationError(f"{model.name} {alg}: constant outputs {bad} other than 0")
@@ -1168,7 +1175,8 @@ def _layout(model, alg, dt, em, device=True):
         row = _odd(base)
         stage = stage_outputs(model, alg, dt, bk)
     return dict(n=n, ext=ext, nin=nin, nsc=nsc, bk=bk, stage=stage, sin=row, sout=sout,
-                plan=plan, minb=minb, park=plan is not None, lo=em.lo, np=em.np, in_layout=em.in_layout)
+                plan=plan, minb=minb, park=plan is not None and plan.park, lo=em.lo, np=em.np,
+                in_layout=em.in_layout)
 
 
 def _input_consts(layout):
