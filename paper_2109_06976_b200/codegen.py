@@ -457,7 +457,7 @@ class _Program:
         return dict(v=v, a=a, f=f, Xv=Xv, Xa=Xa, vJ=vJ, Iv=Iv, tau=tau)
 
     # -- direct Minv (reference refdyn.py:128-169, column-wise) ------------------
-    def emit_minv(self, tree, t=0, store=False):
+    def emit_minv(self, tree, t=0, store=False, on_column=None):
         em = self.em
         em.task = f"ia.{t}"
         IA = {i: [row[:] for row in self.I[i]] for i in tree}
@@ -528,6 +528,8 @@ class _Program:
                     self.store("o0", i * self.n + j, M[(i, j)])
                     if i != j:
                         self.store("o0", j * self.n + i, M[(i, j)])
+            if on_column is not None:
+                on_column(j, M)
         return M, U, Dinv
 
     # -- gradient of ID, column-major (reference refdyn.py:178-239) -------------
@@ -596,13 +598,14 @@ class _Program:
     def store(self, slot, idx, e):
         self.em.store(int(slot[1]), idx, e)
 
-    def run(self, trees=None, zero_fill=True, cols=None, fext=False):
+    def run(self, trees=None, zero_fill=True, cols=None, fext=False, lowmem=False):
         """Emit the whole one-knot program.  Every op carries a task tag:
         'in' / 'xf' (input loads, joint transforms: re-materialised by each
         consumer), then per root tree t: rnea0.t, ia.t, minv.t.j, fd.t,
         rnea1.t, grad.t.<q|qd>.c, zeros.  The thread-per-knot mapping ignores
         the tags; the warp-specialised mapping schedules tasks over warps."""
         alg, n, em = self.alg, self.n, self.em
+        self.lowmem = bool(lowmem)
         part = [t for t in range(len(self.trees)) if trees is None or t in trees]
         dofs = sorted(i for t in part for i in self.trees[t])
         if not dofs or dofs != list(range(dofs[0], dofs[-1] + 1)):
@@ -652,7 +655,7 @@ class _Program:
                     for i in tree:
                         self.store("o2", i, qdd[i])
                 em.task = f"rnea1.{t}"
-                R = self.emit_rnea(tree, qdd, v_in=(R0["v"], R0["Xv"]))
+                R = self.emit_rnea(tree, qdd, v_in=None if self.lowmem else (R0["v"], R0["Xv"]))
                 self.emit_xcf(tree, R)
                 for o, kind in (("o0", "q"), ("o1", "qd")):
                     for c in tree:
@@ -680,6 +683,26 @@ class _Program:
         em = self.em
         em.task = f"rnea0.{t}"
         R0 = self.emit_rnea(tree, None)
+        if self.lowmem:
+            # accumulate qdd column by column as Minv is produced, so Minv
+            # entries die right after use (same products, summed in column order)
+            tau = self.inp["tau"]
+            umc = {i: em.lin([(1.0, tau[i], 1.0), (-1.0, R0["tau"][i], 1.0)], hint="umc") for i in tree}
+            acc = {i: None for i in tree}
+
+            def add(i, m, k):
+                acc[i] = em.lin([(1.0, acc[i], 1.0), (1.0, m, umc[k])], hint="qdd")
+
+            def on_column(j, M):
+                for i in tree:
+                    if i > j:
+                        break
+                    add(i, M[(i, j)], j)
+                    if i != j:
+                        add(j, M[(i, j)], i)
+
+            M, _, _ = self.emit_minv(tree, t, on_column=on_column)
+            return acc, M, R0
         M, _, _ = self.emit_minv(tree, t)
         em.task = f"fd.{t}"
         tau = self.inp["tau"]
@@ -742,7 +765,7 @@ for _a in ALGORITHMS:
         # humanoid30: small batches on the warp-specialised kernel; large ones
         # per root tree (torso tree, two legs)
         TUNED[("humanoid30", _a, _d)] = {"maps": ["ws"], "warps": 16, "minb": 1, "parts": [[0], [1], [2]],
-                                         "zero_memset": True}
+                                         "zero_memset": True, "split": False}
 
 
 def tuning(model=None, alg=None, dtype=None):
@@ -783,11 +806,67 @@ def stage_outputs(model, alg, dtype, bk):
     return bk * _odd(ext) * es <= tuning(model, alg, dtype)["stage_kb"] * 1024
 
 
-def generate_knot(model, alg, dtype, trees=None, zero_fill=True, cols=None, fext=False):
+def generate_knot(model, alg, dtype, trees=None, zero_fill=True, cols=None, fext=False, lowmem=False):
     """The one-knot program as an op list (`_Emit`).  trees: restrict to
     these root trees (a 'part'; its outputs are the trees' blocks);
     zero_fill: also store the structural zeros outside the blocks emitted."""
-    return _Program(model, alg, dtype).run(trees, zero_fill, None if cols is None else frozenset(cols), fext)
+    return _Program(model, alg, dtype).run(trees, zero_fill, None if cols is None else frozenset(cols), fext,
+                                           lowmem)
+
+
+_FLOPS = {"fma": 2, "mul": 1, "add": 1, "sub": 1, "rcp": 1}
+
+
+def _sub_emit(em, ops, tasks):
+    """An _Emit holding a subset of another's ops (same registers, inputs)."""
+    sub = _Emit(em.dtype)
+    sub.ops, sub.tasks, sub.nreg = ops, tasks, em.nreg
+    sub.lo, sub.np, sub.in_layout, sub.in_total, sub.fext = em.lo, em.np, em.in_layout, em.in_total, em.fext
+    sub.flops = sum(_FLOPS.get(op[0], 0) for op in ops)
+    return sub
+
+
+def split_columns(em):
+    """Cut a gradient program into a prefix (RNEA, articulated-inertia
+    factorisation, Minv, FD, RNEA at qdd) and its gradient columns.
+
+    Returns (prefix, columns, nx): `prefix` ends every value the columns
+    import with ("xst", slot, reg) -- a store to the knot's export slot in an
+    L2-resident scratch -- and `columns` starts with ("imp", reg, slot) for
+    each of them; inputs and joint transforms are re-materialised on the
+    column side.  nx = number of export slots."""
+    col = [t.startswith("grad.") for t in em.tasks]
+    remat = ("in", "xf")
+    defs = {}
+    for i, op in enumerate(em.ops):
+        for d in op_dsts(op):
+            defs[d] = i
+    exports = {}
+    for i, op in enumerate(em.ops):
+        if not col[i]:
+            continue
+        for r in op_srcs(op):
+            di = defs[r]
+            if col[di] or em.tasks[di] in remat:
+                continue
+            exports.setdefault(r, len(exports))
+    pops, ptasks = [], []
+    for i, op in enumerate(em.ops):
+        if col[i]:
+            continue
+        pops.append(op)
+        ptasks.append(em.tasks[i])
+        for d in op_dsts(op):
+            if d in exports:
+                pops.append(("xst", exports[d], d))
+                ptasks.append(em.tasks[i])
+    cops = [("imp", r, sl) for r, sl in exports.items()]
+    ctasks = ["imp"] * len(cops)
+    for i, op in enumerate(em.ops):
+        if col[i] or em.tasks[i] in remat:
+            cops.append(op)
+            ctasks.append(em.tasks[i])
+    return _sub_emit(em, pops, ptasks), _sub_emit(em, cops, ctasks), len(exports)
 
 
 def _lit(x, dtype):
@@ -874,7 +953,9 @@ def op_srcs(op):
     k = op[0]
     if k == "st":
         args = op[3:4]
-    elif k in ("ld", "sincos"):
+    elif k == "xst":
+        args = op[2:3]
+    elif k in ("ld", "sincos", "imp"):
         args = ()
     else:
         args = op[2:]
@@ -883,7 +964,7 @@ def op_srcs(op):
 
 def op_dsts(op):
     k = op[0]
-    if k == "st":
+    if k in ("st", "xst"):
         return []
     if k == "sincos":
         return [op[1], op[2]]
@@ -1096,6 +1177,9 @@ def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None
             lines.append(f"neg.{t} {R}{op[1]}, {use(op[2])};")
         elif k == "rcp":
             lines.append(f"rcp.rn.{t} {R}{op[1]}, {use(op[2])};")
+        elif k == "xst":
+            # export to the knot's scratch slot (L2; [32-knot chunk][slot][lane])
+            lines.append(f"st.global.{t} [%5+{op[1] * 32 * es}], {use(op[2])};")
         elif k == "st":
             if plan is not None and plan.park:
                 if not isinstance(op[3], float):  # constants come from the output map
@@ -1240,9 +1324,11 @@ def _omap_decl(L, name):
     return lines
 
 
-def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=False):
-    """Device header: C++ sin/cos prologue + the PTX body in one asm block."""
-    em = generate_knot(model, alg, dt, trees, zero_fill, fext=fext)
+def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=False, em=None, nx=0):
+    """Device header: C++ sin/cos prologue + the PTX body in one asm block.
+    nx > 0: the program exports nx values per knot to the split scratch."""
+    if em is None:
+        em = generate_knot(model, alg, dt, trees, zero_fill, fext=fext)
     L = _layout(model, alg, dt, em)
     n = L["n"]
     space = "shared" if L["stage"] else "global"
@@ -1260,7 +1346,8 @@ def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=Fal
         '#include "rbd_runtime.cuh"',
     ] + ctab.declaration() + _omap_decl(L, name or f"Knot_{alg}_{dt}") \
         + _struct_head(model, alg, dt, L, em.flops, name) + [
-        "  __device__ __forceinline__ static void run_dev(T* my, T* o0, T* o1, T* o2, unsigned valid) {",
+        f"  static constexpr int NX = {nx};  // values exported per knot to the split scratch",
+        "  __device__ __forceinline__ static void run_dev(T* my, T* o0, T* o1, T* o2, unsigned valid, T* xb) {",
     ]
     if L.get("park"):
         nm = name or f"Knot_{alg}_{dt}"
@@ -1276,9 +1363,9 @@ def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=Fal
     if L["stage"]:
         src.append("    const unsigned a0 = (unsigned)__cvta_generic_to_shared(o0), "
                    "a1 = (unsigned)__cvta_generic_to_shared(o1), a2 = (unsigned)__cvta_generic_to_shared(o2);")
-        ops = '"r"(a_in), "r"(a0), "r"(a1), "r"(a2), "r"(valid)'
+        ops = '"r"(a_in), "r"(a0), "r"(a1), "r"(a2), "r"(valid), "l"(xb)'
     else:
-        ops = '"r"(a_in), "l"(o0), "l"(o1), "l"(o2), "r"(valid)'
+        ops = '"r"(a_in), "l"(o0), "l"(o1), "l"(o2), "r"(valid), "l"(xb)'
     src.append('    asm volatile("{\\n\\t"')
     for ln in body:
         src.append(f'      "{ln}\\n\\t"')
@@ -1287,10 +1374,12 @@ def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=Fal
     return "\n".join(src), em.flops, L
 
 
-def _ws_struct(model, alg, dt, warps, name=None, trees=None, zero_fill=True, fext=False):
-    """Device header of the warp-specialised mapping (see wsched.py)."""
+def _ws_struct(model, alg, dt, warps, name=None, trees=None, zero_fill=True, fext=False, em=None):
+    """Device header of the warp-specialised mapping (see wsched.py).  With
+    an `em` holding "imp" ops (split columns), the arena is the per-group
+    slice of the split scratch the prefix kernel filled."""
     from . import wsched
-    P = wsched.plan(model, alg, dt, warps, trees, zero_fill, fext)
+    P = wsched.plan(model, alg, dt, warps, trees, zero_fill, fext, em=em)
     em, sched = P["em"], P["sched"]
     n, nin = P["n"], P["nin"]
     T = "double" if dt == "f64" else "float"
@@ -1317,6 +1406,8 @@ def _ws_struct(model, alg, dt, warps, name=None, trees=None, zero_fill=True, fex
         f"  static constexpr int SIN = {P['sin']}, NA = {sched.nslots}, SOUT = {P['sout']};",
         f"  static constexpr bool STAGE = {'true' if P['stage'] else 'false'}, "
         f"ARENA_SMEM = {'true' if P['arena_smem'] else 'false'};",
+        f"  static constexpr bool ARENA_GROUP = {'true' if P.get('imports') else 'false'};"
+        "  // arena = the group's slice of the split scratch",
         f"  static constexpr int FLOPS = {em.flops};",
         f"  static constexpr int MINB = {int(tuning(model, alg, dt).get('minb', 1))};  // min CTAs per SM (register cap)",
         "  typedef " + AT + " arena_t;",
@@ -1399,6 +1490,32 @@ def _launch_unit(alg, dt, tag, K, text):
     ])
 
 
+def _big_part_unit(model, alg, dt, tag, K, tn, trees, zero_fill, fx):
+    """A part whose one-knot program does not fit a thread.  Gradient
+    programs are split (`split_columns`): a thread-per-knot prefix kernel
+    exporting to an L2-resident scratch + a one-phase warp-specialised column
+    kernel reading it; other algorithms run warp-specialised as a whole."""
+    if alg in ("gradID", "gradFD") and tn.get("split", True):
+        em = generate_knot(model, alg, dt, trees, zero_fill, fext=fx, lowmem=True)
+        pre, cols, nx = split_columns(em)
+        try:
+            ta, _, _ = _knot_struct(model, alg, dt, K + "A", em=pre, nx=nx)
+            tb, _, _ = _ws_struct(model, alg, dt, int(tn["warps"]), K + "B", em=cols)
+            return "\n".join([
+                ta.replace("#pragma once\n", ""), tb.replace("#pragma once\n", ""),
+                f'extern "C" int rbd__launch_{alg}_{dt}_{tag}(const void* q, const void* qd, const void* u, '
+                "const void* fx,",
+                "                                void* o0, void* o1, void* o2, int64_t N, void* stream) {",
+                f"  return rbd_launch_split<{K}A, {K}B>(q, qd, u, fx, o0, o1, o2, N, stream);",
+                "}",
+                "",
+            ])
+        except GenerationError:
+            pass
+    text, _, _ = _ws_struct(model, alg, dt, int(tn["warps"]), K, trees=trees, zero_fill=zero_fill, fext=fx)
+    return _launch_unit(alg, dt, tag, K, text)
+
+
 def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
     """{file name: text} of the per-robot library plus {(alg, dtype): flops}.
 
@@ -1450,10 +1567,10 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
                     try:
                         text, fl, L = _knot_struct(model, alg, dt, K, trees=tuple(trees), zero_fill=zf and pi == 0,
                                                    fext=fx)
+                        files[f"k_{alg}_{dt}_{tag}.cu"] = _launch_unit(alg, dt, tag, K, text)
                     except GenerationError:
-                        text, fl, L = _ws_struct(model, alg, dt, int(tn["warps"]), K, trees=tuple(trees),
-                                                 zero_fill=zf and pi == 0, fext=fx)
-                    files[f"k_{alg}_{dt}_{tag}.cu"] = _launch_unit(alg, dt, tag, K, text)
+                        files[f"k_{alg}_{dt}_{tag}.cu"] = _big_part_unit(model, alg, dt, tag, K, tn, tuple(trees),
+                                                                         zf and pi == 0, fx)
                     ptags.append(tag)
                 for tag in tags + ptags:
                     dispatch.append(f'extern "C" int rbd__launch_{alg}_{dt}_{tag}{sig}')

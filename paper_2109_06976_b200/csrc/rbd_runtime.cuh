@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(K::BK, K::MINB)
 rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __restrict__ qd,
                  const typename K::T* __restrict__ u, const typename K::T* __restrict__ fx,
                  typename K::T* __restrict__ o0, typename K::T* __restrict__ o1,
-                 typename K::T* __restrict__ o2, long long N) {
+                 typename K::T* __restrict__ o2, long long N, typename K::T* __restrict__ xs) {
   typedef typename K::T T;
   constexpr int BK = K::BK, n = K::NDOF;
   extern __shared__ __align__(16) unsigned char rbd_smem[];
@@ -127,11 +127,13 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
   }
   __syncthreads();
   T* my = s_in + tid * K::SIN;  // this knot's inputs + its sin/cos scratch
+  // split prefix kernel: this knot's export slots in the scratch ([32-knot chunk][slot][lane])
+  T* xb = K::NX ? xs + ((size_t)((base + tid) >> 5) * K::NX * 32 + ((base + tid) & 31)) : nullptr;
 
   if constexpr (K::PARK) {
     // the program parks every output value in its row; write the CTA's
     // contiguous output ranges back coalesced (structural zeros from the map)
-    K::run_dev(my, nullptr, nullptr, nullptr, 1u);
+    K::run_dev(my, nullptr, nullptr, nullptr, 1u, xb);
     __syncthreads();
     if constexpr (!rbd_ofull<K>()) {
       // a part program (subset of the root trees): only its own elements
@@ -162,7 +164,7 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
     }
   } else if constexpr (K::STAGE) {
     T* o = s_out + tid * K::SOUT;
-    K::run_dev(my, o, o + K::E0, o + K::E0 + K::E1, 1u);
+    K::run_dev(my, o, o + K::E0, o + K::E0 + K::E1, 1u, xb);
     __syncthreads();
     // coalesced write-back, one output array at a time
     {
@@ -191,7 +193,7 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
     // padding threads of the last CTA are predicated off
     const long long k = base + (tid < nk ? tid : 0);
     K::run_dev(my, o0 + k * K::E0, K::E1 ? o1 + k * K::E1 : nullptr,
-               K::E2 ? o2 + k * K::E2 : nullptr, tid < nk ? 1u : 0u);
+               K::E2 ? o2 + k * K::E2 : nullptr, tid < nk ? 1u : 0u, xb);
   }
 }
 
@@ -251,6 +253,8 @@ rbd_ws_kernel(const typename K::T* __restrict__ q, const typename K::T* __restri
     typename K::arena_t a_ar;
     if constexpr (K::ARENA_SMEM)
       a_ar = (unsigned)__cvta_generic_to_shared(s_ar + lane);
+    else if constexpr (K::ARENA_GROUP)  // split columns: the prefix kernel's exports of this group
+      a_ar = (unsigned long long)(garena + (size_t)g * K::NA * 32 + lane);
     else
       a_ar = (unsigned long long)(garena + (size_t)blockIdx.x * K::NA * 32 + lane);
     typename K::out_t a0, a1, a2;
@@ -311,7 +315,7 @@ struct rbd_dev_cache {
 
 template <class K>
 static int rbd_launch_kernel(const void* q, const void* qd, const void* u, const void* fx, void* o0,
-                             void* o1, void* o2, int64_t N, void* stream) {
+                             void* o1, void* o2, int64_t N, void* stream, void* xs = nullptr) {
   typedef typename K::T T;
   if (N < 0) return RBD_EINVAL;
   if (N == 0) return 0;
@@ -346,7 +350,7 @@ static int rbd_launch_kernel(const void* q, const void* qd, const void* u, const
       if (e != cudaSuccess) return (int)e;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       c.grid = (per_sm > 0 ? per_sm : 1) * sms;
-      if (!K::ARENA_SMEM) {
+      if (!K::ARENA_SMEM && !K::ARENA_GROUP) {
         c.arena_bytes = sizeof(T) * (size_t)c.grid * K::NA * 32;
         e = cudaMalloc(&c.arena, c.arena_bytes);
         if (e != cudaSuccess) { c.grid = 0; return (int)e; }
@@ -354,15 +358,60 @@ static int rbd_launch_kernel(const void* q, const void* qd, const void* u, const
     }
     const long long groups = (N + 31) / 32;
     const long long grid = groups < c.grid ? groups : c.grid;
+    if (K::ARENA_GROUP && !xs) return RBD_EINVAL;
     rbd_ws_kernel<K><<<(unsigned)grid, K::W * 32, smem, (cudaStream_t)stream>>>(
         (const T*)q, (const T*)qd, (const T*)u, (const T*)fx, (T*)o0, (T*)o1, (T*)o2, (long long)N,
-        (T*)c.arena);
+        K::ARENA_GROUP ? (T*)xs : (T*)c.arena);
   } else {
     const long long grid = (N + K::BK - 1) / K::BK;
+    if (K::NX && !xs) return RBD_EINVAL;
     rbd_batch_kernel<K><<<(unsigned)grid, K::BK, smem, (cudaStream_t)stream>>>(
-        (const T*)q, (const T*)qd, (const T*)u, (const T*)fx, (T*)o0, (T*)o1, (T*)o2, (long long)N);
+        (const T*)q, (const T*)qd, (const T*)u, (const T*)fx, (T*)o0, (T*)o1, (T*)o2, (long long)N,
+        (T*)xs);
   }
   return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// split gradient program (large root trees): the prefix kernel KA (thread per
+// knot: RNEA, articulated inertias, Minv, FD, RNEA at qdd) exports the values
+// the gradient columns need to a scratch; the column kernel KB (warp-
+// specialised, one phase, no barriers between columns) reads them as its
+// arena.  Chunks of RBD_SPLIT_CHUNK knots keep the scratch L2-resident.
+// ---------------------------------------------------------------------------
+#define RBD_SPLIT_CHUNK 16384
+template <class KA, class KB>
+static int rbd_launch_split(const void* q, const void* qd, const void* u, const void* fx, void* o0,
+                            void* o1, void* o2, int64_t N, void* stream) {
+  typedef typename KA::T T;
+  static_assert(KA::NX == KB::NA, "prefix exports and column imports disagree");
+  static_assert(RBD_SPLIT_CHUNK % KA::BK == 0 && KA::BK % 32 == 0, "chunk / CTA / warp alignment");
+  if (N < 0) return RBD_EINVAL;
+  if (N == 0) return 0;
+  static void* scratch[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!scratch[dev & 63]) {
+    cudaError_t e = cudaMalloc(&scratch[dev & 63], sizeof(T) * (size_t)RBD_SPLIT_CHUNK * KA::NX);
+    if (e != cudaSuccess) return (int)e;
+  }
+  void* xs = scratch[dev & 63];
+  constexpr int n = KA::NDOF;
+  for (int64_t c0 = 0; c0 < N; c0 += RBD_SPLIT_CHUNK) {
+    const int64_t nk = (N - c0) < RBD_SPLIT_CHUNK ? (N - c0) : RBD_SPLIT_CHUNK;
+    const T* cq = (const T*)q + c0 * n;
+    const T* cqd = qd ? (const T*)qd + c0 * n : nullptr;
+    const T* cu = u ? (const T*)u + c0 * n : nullptr;
+    const T* cfx = fx ? (const T*)fx + c0 * 6 * n : nullptr;
+    T* c_o0 = (T*)o0 + c0 * KA::E0;
+    T* c_o1 = KA::E1 ? (T*)o1 + c0 * KA::E1 : nullptr;
+    T* c_o2 = KA::E2 ? (T*)o2 + c0 * KA::E2 : nullptr;
+    int rc = rbd_launch_kernel<KA>(cq, cqd, cu, cfx, c_o0, c_o1, c_o2, nk, stream, xs);
+    if (rc) return rc;
+    rc = rbd_launch_kernel<KB>(cq, cqd, cu, cfx, c_o0, c_o1, c_o2, nk, stream, xs);
+    if (rc) return rc;
+  }
+  return 0;
 }
 
 // ---------------------------------------------------------------------------

@@ -66,12 +66,17 @@ class Schedule:
         self.em = em
         ops, tags = em.ops, em.tasks
         self.def_op = {}
+        imported = {}  # reg -> fixed arena slot (split columns: the prefix kernel's exports)
         for i, op in enumerate(ops):
+            if op[0] == "imp":
+                self.def_op[op[1]] = i
+                imported[op[1]] = op[2]
+                continue
             for r in _dsts(op):
                 self.def_op[r] = i
         self.task_ops = defaultdict(list)
         for i, t in enumerate(tags):
-            if not _remat(t):
+            if not _remat(t) and t != "imp":
                 self.task_ops[t].append(i)
         # cross-task values and dependencies
         self.export = {}  # reg -> producing task
@@ -81,7 +86,7 @@ class Schedule:
             for i in idxs:
                 for r in _srcs(ops[i]):
                     dt = tags[self.def_op[r]]
-                    if _remat(dt) or dt == t:
+                    if _remat(dt) or dt == t or dt == "imp":
                         continue
                     self.export[r] = dt
                     deps[t].add(dt)
@@ -124,8 +129,9 @@ class Schedule:
             b = max(level[u] for u in users[r])
             iv.append((a, b, r))
         iv.sort()
-        slot_end = []  # per slot: last phase it is read in
-        self.slot = {}
+        nimp = 1 + max(imported.values()) if imported else 0
+        slot_end = [1 << 30] * nimp  # per slot: last phase it is read in (imports: never recycled)
+        self.slot = dict(imported)
         for a, b, r in iv:
             for s, e in enumerate(slot_end):
                 if e < a:
@@ -264,10 +270,12 @@ def ptx_block(sched, tasks, dtype, scratch_base, nin_slots, arena_space, out_spa
     return head + lines
 
 
-def plan(model, alg, dtype, warps, trees=None, zero_fill=True, fext=False):
+def plan(model, alg, dtype, warps, trees=None, zero_fill=True, fext=False, em=None):
     """Schedule + memory plan of the warp-specialised kernel."""
-    em = cg.generate_knot(model, alg, dtype, trees, zero_fill, fext=fext)
+    if em is None:
+        em = cg.generate_knot(model, alg, dtype, trees, zero_fill, fext=fext)
     sched = Schedule(em, warps)
+    imports = any(op[0] == "imp" for op in em.ops)
     n = model.n_dof
     es = 8 if dtype == "f64" else 4
     nin = len(em.in_layout)
@@ -278,11 +286,11 @@ def plan(model, alg, dtype, warps, trees=None, zero_fill=True, fext=False):
     row = LANES * es
     sout = sum(ext)
     opts = [(True, True), (True, False), (False, True), (False, False)]  # (arena smem, stage outputs)
-    if cg.tuning(model, alg, dtype).get("arena") == "global":
+    if cg.tuning(model, alg, dtype).get("arena") == "global" or imports:
         opts = [(False, True), (False, False)]
     for ar, st in opts:
         smem = row * (sin + (sched.nslots if ar else 0) + (sout if st else 0))
         if smem <= SMEM_BUDGET:
             break
     return dict(em=em, sched=sched, n=n, nin=nin, nsc=nsc, ext=ext, sin=sin, sout=sout,
-                arena_smem=ar, stage=st, smem=smem, es=es, warps=warps)
+                arena_smem=ar, stage=st, smem=smem, es=es, warps=warps, imports=imports)

@@ -234,3 +234,62 @@ def test_device_ptx_with_fext(name, mapping):
             outs, _ = run_ws(m, alg, "f64", x, warps=5, arena_space="global", out_space="global", fext=True)
         for (nm, _), o in zip(codegen.outputs(alg, n), outs):
             assert rel_err(o[None], g[f"fext.{alg}.{nm}"][3:4]) < 1e-12, (name, alg, nm)
+
+
+@pytest.mark.parametrize("name,trees", [("humanoid30", (0,)), ("chain7", None), ("quad12", None)])
+@pytest.mark.parametrize("alg", ["gradID", "gradFD"])
+def test_split_prefix_and_columns(name, trees, alg):
+    """Split gradient program (large root trees): the prefix kernel's PTX
+    (register plan, exports stored to the knot's scratch slots) followed by
+    the one-phase column kernel's PTX (imports read from that scratch as its
+    arena) reproduces the reference."""
+    g = golden(name)
+    m = models.load(name)
+    n = m.n_dof
+    k = 4
+    em = codegen.generate_knot(m, alg, "f64", trees, trees is None, lowmem=True)
+    pre, cols, nx = codegen.split_columns(em)
+    lo, np_ = em.lo, em.np
+    x_full = _inputs(g, alg, k, n)
+    x = np.concatenate([x_full[a * n + lo:a * n + lo + np_] for a in range(3)])
+    # prefix: thread-per-knot with its register plan
+    nsc = len(_sincos_slots(pre))
+    plan = codegen.SpillPlan(pre, 48, codegen.row_homes(pre, pre.in_total), pre.in_total + 2 * nsc, park_outputs=True)
+    ctab = codegen.ConstTable("K", "f64")
+    lines, sc = codegen.ptx_body(pre, pre.in_total, "global", ctab=ctab, plan=plan)
+    row = {i: float(v) for i, v in enumerate(x)}
+    for j, slot in enumerate(sc):
+        row[pre.in_total + 2 * j] = math.sin(x[slot])
+        row[pre.in_total + 2 * j + 1] = math.cos(x[slot])
+    scratch = {}
+    ptxsim.run_block(lines, [row, {}, {}, {}, None, scratch], [8, 8, 8, 8, 8, 32 * 8],
+                     consts={"K": sorted(ctab.index, key=ctab.index.get)})
+    assert len(scratch) == nx
+    outs = [dict() for _ in range(3)]
+    for (kk, idx), sl in plan.outslot.items():
+        outs[kk][idx] = row[sl]
+    for (kk, idx), v in plan.outconst.items():
+        outs[kk][idx] = v
+    # columns: one phase, arena = the scratch
+    P = wsched.plan(m, alg, "f64", 6, em=cols)
+    S = P["sched"]
+    assert len(S.phases) == 1 and S.nslots >= nx
+    L = wsched.LANES
+    srow = {i: float(v) for i, v in enumerate(x)}
+    for j, slot in enumerate(_sincos_slots(cols)):
+        srow[cols.in_total + 2 * j] = math.sin(x[slot])
+        srow[cols.in_total + 2 * j + 1] = math.cos(x[slot])
+    ctab = codegen.ConstTable("K", "f64")
+    for tasks in S.phases[0]:
+        if tasks:
+            lines = wsched.ptx_block(S, tasks, "f64", cols.in_total, cols.in_total, "global", "global", 0, ctab)
+            ptxsim.run_block(lines, [srow, scratch] + outs + [None], [L * 8, 32 * 8, 8, 8, 8],
+                             consts={"K": sorted(ctab.index, key=ctab.index.get)})
+    owned = set(range(lo, lo + np_))
+    for (nm, e), o in zip(codegen.outputs(alg, n), outs):
+        ref = g[f"{alg}.{nm}"][k]
+        idx = [i for i in range(e) if (i // n in owned and i % n in owned) if e == n * n] or \
+              [i for i in range(e) if i in owned]
+        got = np.array([o.get(i, np.nan) for i in idx])
+        assert np.all(np.isfinite(got)), (name, alg, nm)
+        assert rel_err(got[None], ref[idx][None]) < 1e-12, (name, alg, nm)
