@@ -750,6 +750,8 @@ TUNING_DEFAULT = {
     "warps_per_sm": 16,  # thread + ra: target occupancy (lowered until the row fits)
     "park": True,        # thread + ra: park outputs in the row, coalesced write-back
     "ra_budget": 0,      # thread + ra: cap on values kept in registers (0: from the register cap)
+    "prefetch_dist": 0,  # thread + ra: issue reloads up to this many ops before use (0: at use)
+    "prefetch_slack": 0,  # ... with at most this many prefetched values in flight
 }
 TUNED = {}
 # measured on B200 (N = 2^20): chain7 gradFD fp64 is compute-bound at 6 warps/SM
@@ -765,7 +767,7 @@ for _a in ALGORITHMS:
         # humanoid30: small batches on the warp-specialised kernel; large ones
         # per root tree (torso tree, two legs)
         TUNED[("humanoid30", _a, _d)] = {"maps": ["ws"], "warps": 16, "minb": 1, "parts": [[0], [1], [2]],
-                                         "zero_memset": True, "split": False}
+                                         "zero_memset": True, "split": True}
 
 
 def tuning(model=None, alg=None, dtype=None):
@@ -989,11 +991,14 @@ class SpillPlan:
     Result: before[i] = values to (re)load before op i, after[i] = (value,
     slot) stores after op i, slot[v] = row slot of v, nslots = row length."""
 
-    def __init__(self, em, budget, homes, reserved, park_outputs=False, flushes=()):
+    def __init__(self, em, budget, homes, reserved, park_outputs=False, flushes=(), prefetch=None):
         """flushes: (op index, output k) pairs: before that op the CTA writes
-        output k back and its parked slots are recycled."""
+        output k back and its parked slots are recycled.  Values defined by
+        ("imp", reg, slot) ops (split columns) live in the global scratch:
+        evicting them is free, reloading them reads slot `gslot[reg]`."""
         ops = em.ops
         self.park = park_outputs
+        self.gslot = {op[1]: op[2] for op in ops if op[0] == "imp"}
         fl = {}
         for i, k in flushes:
             fl.setdefault(i, []).append(k)
@@ -1013,6 +1018,8 @@ class SpillPlan:
         self.after = {}
         self.reloads = self.stores = 0
         far = 1 << 40
+        evicted_at = {}   # value -> op index of its last eviction
+        reload_log = []   # (value, op index it is needed at, earliest issue point)
 
         def next_use(v):
             p = ptr[v]
@@ -1027,9 +1034,10 @@ class SpillPlan:
             srcs = op_srcs(op)
             for a in srcs:
                 if a not in inreg:
-                    if a not in self.slot:
+                    if a not in self.slot and a not in self.gslot:
                         raise GenerationError(f"value {a} used before it is defined")
                     self.before.setdefault(i, []).append(a)
+                    reload_log.append((a, i, evicted_at.get(a, 0)))
                     self.reloads += 1
                     inreg.add(a)
             if park_outputs and op[0] == "st":
@@ -1050,14 +1058,15 @@ class SpillPlan:
                     if sl is not None and sl in occupied:
                         occupied.discard(sl)
                         heapq.heappush(free, sl)
-            if op[0] not in ("ld", "sincos"):
+            if op[0] not in ("ld", "sincos", "imp"):
                 for d in op_dsts(op):
                     if d in uses:
                         inreg.add(d)
             while len(inreg) > budget:
-                v = max(inreg, key=lambda x: (next_use(x), x in self.slot))
+                v = max(inreg, key=lambda x: (next_use(x), x in self.slot or x in self.gslot))
                 inreg.discard(v)
-                if v not in self.slot:
+                evicted_at[v] = i + 1
+                if v not in self.slot and v not in self.gslot:
                     sl = heapq.heappop(free) if free else top
                     if sl == top:
                         top += 1
@@ -1066,6 +1075,26 @@ class SpillPlan:
                     self.after.setdefault(i, []).append((v, sl))
                     self.stores += 1
         self.nslots = top
+        if prefetch:
+            self._prefetch(reload_log, len(ops), *prefetch)
+
+    def _prefetch(self, reload_log, nops, dist, slack):
+        """Issue each reload up to `dist` ops before its use (never before the
+        value left its register), keeping at most `slack` prefetched values
+        in flight at any op: the plan ran with `budget` registers, the
+        kernel has budget + slack, so load latency (L2 for split-column
+        imports, shared memory otherwise) overlaps the arithmetic."""
+        extra = [0] * (nops + 1)
+        self.before = {}
+        for a, i, lo in reload_log:
+            j = max(lo, i - dist, 0)
+            for k in range(i - 1, j - 1, -1):
+                if extra[k] >= slack:
+                    j = k + 1
+                    break
+            for k in range(j, i):
+                extra[k] += 1
+            self.before.setdefault(j, []).append(a)
 
 
 def row_homes(em, scratch_base):
@@ -1138,11 +1167,14 @@ def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None
         step += 1
         if plan is not None:
             for a in plan.before.get(i, ()):
-                lines.append(f"ld.shared.{t} {R}{a}, [%0+{plan.slot[a] * es}];")
+                if a in plan.gslot:  # split columns: import from the knot's scratch slot (L2)
+                    lines.append(f"ld.global.{t} {R}{a}, [%5+{plan.gslot[a] * 32 * es}];")
+                else:
+                    lines.append(f"ld.shared.{t} {R}{a}, [%0+{plan.slot[a] * es}];")
             if k == "sincos":
                 sc.append(op[3])
                 continue
-            if k == "ld":
+            if k in ("ld", "imp"):
                 continue
         if k == "ld":
             home[op[1]] = op[2] * es
@@ -1210,7 +1242,7 @@ CTA_SMEM_RESERVED = 1024  # per-CTA system reservation
 REG_OVERHEAD = 16         # registers ptxas needs besides the budgeted values
 
 
-def _layout(model, alg, dt, em, device=True):
+def _layout(model, alg, dt, em, device=True, over=None):
     """Thread-per-knot launch shape and row layout.
 
     Without the allocator ("ra": false) the row is [inputs | sin/cos] and
@@ -1224,6 +1256,7 @@ def _layout(model, alg, dt, em, device=True):
     nin = len(em.in_layout)
     nsc = sum(1 for op in em.ops if op[0] == "sincos")
     tn = tuning(model, alg, dt)
+    tn.update(over or {})
     bk = int(tn["bk"])
     es = 8 if dt == "f64" else 4
     base = em.in_total + 2 * nsc
@@ -1240,9 +1273,13 @@ def _layout(model, alg, dt, em, device=True):
             budget = (regs - REG_OVERHEAD) // (2 if dt == "f64" else 1)
             if tn.get("ra_budget"):
                 budget = min(budget, int(tn["ra_budget"]))
+            pf = None
+            if tn.get("prefetch_dist"):
+                pf = (int(tn["prefetch_dist"]), int(tn["prefetch_slack"]))
+                budget -= pf[1]
             park = bool(tn.get("park", True))
             row_max = (SM_SMEM - ctas * (CTA_SMEM_RESERVED + (4 * sum(ext) if park else 0) + 16)) // (threads * es)
-            plan = SpillPlan(em, budget, homes, base, park_outputs=park)
+            plan = SpillPlan(em, budget, homes, base, park_outputs=park, prefetch=pf)
             if _odd(plan.nslots) <= row_max:
                 minb = ctas
                 break
@@ -1317,19 +1354,20 @@ def _omap_decl(L, name):
     if sum(L["ext"]) > 65535:
         raise GenerationError(f"{name}: output map too large")
     L["nout"], L["ofull"] = len(om), full
-    lines = [f"__constant__ short rbd_om_{name}[{len(om)}] = {{{', '.join(str(sl) for _, sl in om)}}};"]
+    pad = om or [(0, -1)]  # a program with no outputs (split gradID prefix) keeps a 1-entry dummy map
+    lines = [f"__constant__ short rbd_om_{name}[{len(pad)}] = {{{', '.join(str(sl) for _, sl in pad)}}};"]
     if not full:
-        lines.append(f"__constant__ unsigned short rbd_oe_{name}[{len(om)}] = "
-                     f"{{{', '.join(str(e) for e, _ in om)}}};")
+        lines.append(f"__constant__ unsigned short rbd_oe_{name}[{len(pad)}] = "
+                     f"{{{', '.join(str(e) for e, _ in pad)}}};")
     return lines
 
 
-def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=False, em=None, nx=0):
+def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=False, em=None, nx=0, over=None):
     """Device header: C++ sin/cos prologue + the PTX body in one asm block.
     nx > 0: the program exports nx values per knot to the split scratch."""
     if em is None:
         em = generate_knot(model, alg, dt, trees, zero_fill, fext=fext)
-    L = _layout(model, alg, dt, em)
+    L = _layout(model, alg, dt, em, over=over)
     n = L["n"]
     space = "shared" if L["stage"] else "global"
     tn = tuning(model, alg, dt)
@@ -1493,14 +1531,19 @@ def _launch_unit(alg, dt, tag, K, text):
 def _big_part_unit(model, alg, dt, tag, K, tn, trees, zero_fill, fx):
     """A part whose one-knot program does not fit a thread.  Gradient
     programs are split (`split_columns`): a thread-per-knot prefix kernel
-    exporting to an L2-resident scratch + a one-phase warp-specialised column
-    kernel reading it; other algorithms run warp-specialised as a whole."""
+    exporting to an L2-resident scratch + a thread-per-knot column kernel
+    whose register plan reloads the imports from that scratch; other
+    algorithms run warp-specialised as a whole."""
     if alg in ("gradID", "gradFD") and tn.get("split", True):
         em = generate_knot(model, alg, dt, trees, zero_fill, fext=fx, lowmem=True)
         pre, cols, nx = split_columns(em)
         try:
             ta, _, _ = _knot_struct(model, alg, dt, K + "A", em=pre, nx=nx)
-            tb, _, _ = _ws_struct(model, alg, dt, int(tn["warps"]), K + "B", em=cols)
+            # the column kernel writes its n x 2 n outputs per knot as it goes
+            # (parking them would need ~4 KB of row per knot)
+            tb, _, _ = _knot_struct(model, alg, dt, K + "B", em=cols, nx=nx,
+                                    over={"park": False, "prefetch_dist": int(tn.get("split_pf_dist", 96)),
+                                          "prefetch_slack": int(tn.get("split_pf_slack", 12))})
             return "\n".join([
                 ta.replace("#pragma once\n", ""), tb.replace("#pragma once\n", ""),
                 f'extern "C" int rbd__launch_{alg}_{dt}_{tag}(const void* q, const void* qd, const void* u, '
@@ -1567,6 +1610,9 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
                     try:
                         text, fl, L = _knot_struct(model, alg, dt, K, trees=tuple(trees), zero_fill=zf and pi == 0,
                                                    fext=fx)
+                        if (L["minb"] * L["bk"] < 32 * int(tn.get("min_warps", 4)) and alg in ("gradID", "gradFD")
+                                and tn.get("split")):
+                            raise GenerationError("thread-per-knot occupancy too low; split the program")
                         files[f"k_{alg}_{dt}_{tag}.cu"] = _launch_unit(alg, dt, tag, K, text)
                     except GenerationError:
                         files[f"k_{alg}_{dt}_{tag}.cu"] = _big_part_unit(model, alg, dt, tag, K, tn, tuple(trees),

@@ -135,7 +135,9 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
     // contiguous output ranges back coalesced (structural zeros from the map)
     K::run_dev(my, nullptr, nullptr, nullptr, 1u, xb);
     __syncthreads();
-    if constexpr (!rbd_ofull<K>()) {
+    if constexpr (rbd_nout<K>() == 0) {
+      // nothing parked (a split prefix whose outputs all come from the columns)
+    } else if constexpr (!rbd_ofull<K>()) {
       // a part program (subset of the root trees): only its own elements
       constexpr int M = rbd_nout<K>();
       for (int idx = tid; idx < nk * M; idx += BK) {
@@ -379,12 +381,12 @@ static int rbd_launch_kernel(const void* q, const void* qd, const void* u, const
 // specialised, one phase, no barriers between columns) reads them as its
 // arena.  Chunks of RBD_SPLIT_CHUNK knots keep the scratch L2-resident.
 // ---------------------------------------------------------------------------
-#define RBD_SPLIT_CHUNK 16384
+#define RBD_SPLIT_CHUNK 32768
 template <class KA, class KB>
 static int rbd_launch_split(const void* q, const void* qd, const void* u, const void* fx, void* o0,
                             void* o1, void* o2, int64_t N, void* stream) {
   typedef typename KA::T T;
-  static_assert(KA::NX == KB::NA, "prefix exports and column imports disagree");
+  static_assert(KA::NX == KB::NX && KA::MAP == 0 && KB::MAP == 0, "prefix exports and column imports disagree");
   static_assert(RBD_SPLIT_CHUNK % KA::BK == 0 && KA::BK % 32 == 0, "chunk / CTA / warp alignment");
   if (N < 0) return RBD_EINVAL;
   if (N == 0) return 0;

@@ -270,6 +270,18 @@ def test_split_prefix_and_columns(name, trees, alg):
         outs[kk][idx] = row[sl]
     for (kk, idx), v in plan.outconst.items():
         outs[kk][idx] = v
+    # columns, thread-per-knot: imports reloaded from the scratch, prefetched
+    cplan = codegen.SpillPlan(cols, 40, codegen.row_homes(cols, cols.in_total),
+                              cols.in_total + 2 * len(_sincos_slots(cols)), prefetch=(48, 6))
+    ctab = codegen.ConstTable("K", "f64")
+    lines, sc = codegen.ptx_body(cols, cols.in_total, "global", ctab=ctab, plan=cplan)
+    crow = {i: float(v) for i, v in enumerate(x)}
+    for j, slot in enumerate(sc):
+        crow[cols.in_total + 2 * j] = math.sin(x[slot])
+        crow[cols.in_total + 2 * j + 1] = math.cos(x[slot])
+    touts = [dict(o) for o in outs]
+    ptxsim.run_block(lines, [crow] + touts + [None, dict(scratch)], [8, 8, 8, 8, 8, 32 * 8],
+                     consts={"K": sorted(ctab.index, key=ctab.index.get)})
     # columns: one phase, arena = the scratch
     P = wsched.plan(m, alg, "f64", 6, em=cols)
     S = P["sched"]
@@ -286,10 +298,11 @@ def test_split_prefix_and_columns(name, trees, alg):
             ptxsim.run_block(lines, [srow, scratch] + outs + [None], [L * 8, 32 * 8, 8, 8, 8],
                              consts={"K": sorted(ctab.index, key=ctab.index.get)})
     owned = set(range(lo, lo + np_))
-    for (nm, e), o in zip(codegen.outputs(alg, n), outs):
-        ref = g[f"{alg}.{nm}"][k]
-        idx = [i for i in range(e) if (i // n in owned and i % n in owned) if e == n * n] or \
-              [i for i in range(e) if i in owned]
-        got = np.array([o.get(i, np.nan) for i in idx])
-        assert np.all(np.isfinite(got)), (name, alg, nm)
-        assert rel_err(got[None], ref[idx][None]) < 1e-12, (name, alg, nm)
+    for variant in (outs, touts):
+        for (nm, e), o in zip(codegen.outputs(alg, n), variant):
+            ref = g[f"{alg}.{nm}"][k]
+            idx = [i for i in range(e) if (i // n in owned and i % n in owned) if e == n * n] or \
+                  [i for i in range(e) if i in owned]
+            got = np.array([o.get(i, np.nan) for i in idx])
+            assert np.all(np.isfinite(got)), (name, alg, nm)
+            assert rel_err(got[None], ref[idx][None]) < 1e-12, (name, alg, nm)

@@ -1,2 +1,2 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "humanoid30" 2>&1 | tail -2
-for dt in f64 f32; do python tools/time_kernel.py --robot humanoid30 --alg gradFD --dtype $dt --n 65536 262144 | cut -c1-150; done
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+for alg in gradFD gradID; do for dt in f64 f32; do python tools/time_kernel.py --robot humanoid30 --alg $alg --dtype $dt --n 262144 | cut -c1-150; done; done
