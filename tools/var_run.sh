@@ -1,2 +1,5 @@
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for alg in gradFD gradID; do for dt in f64 f32; do python tools/time_kernel.py --robot humanoid30 --alg $alg --dtype $dt --n 262144 | cut -c1-150; done; done
+for dt in f64 f32; do VARIANTS=tools/variants_c7.txt bash tools/variants.sh time chain7 gradFD $dt 1048576 2>&1 | python -c "
+import sys, json
+for l in sys.stdin:
+    try: d=json.loads(l); print(d['dtype'], d['tuning'], round(d['us'],1), '%.3g'%d['knots_per_s'])
+    except Exception: print(l[:200])"; done
