@@ -767,7 +767,10 @@ for _a in ALGORITHMS:
         # humanoid30: small batches on the warp-specialised kernel; large ones
         # per root tree (torso tree, two legs)
         TUNED[("humanoid30", _a, _d)] = {"maps": ["ws"], "warps": 16, "minb": 1, "parts": [[0], [1], [2]],
-                                         "zero_memset": True, "split": True}
+                                         "zero_memset": True, "split": True,
+                                         # measured at N = 2^18: per-column programs win in fp32
+                                         # (4.6 -> 4.3 ms), lose in fp64 (7.6 -> 8.4 ms)
+                                         "split_by_task": _d == "f32"}
 
 
 def tuning(model=None, alg=None, dtype=None):
@@ -828,7 +831,7 @@ def _sub_emit(em, ops, tasks):
     return sub
 
 
-def split_columns(em):
+def split_columns(em, by_task=False):
     """Cut a gradient program into a prefix (RNEA, articulated-inertia
     factorisation, Minv, FD, RNEA at qdd) and its gradient columns.
 
@@ -836,22 +839,38 @@ def split_columns(em):
     import with ("xst", slot, reg) -- a store to the knot's export slot in an
     L2-resident scratch -- and `columns` starts with ("imp", reg, slot) for
     each of them; inputs and joint transforms are re-materialised on the
-    column side.  nx = number of export slots."""
+    column side.  nx = number of export slots.
+
+    by_task: `columns` is a list with one program per gradient column task;
+    the joints' sin/cos are exported too (each column program would otherwise
+    evaluate every joint's sincos), and each program keeps only the input
+    loads / transform entries its column uses."""
     col = [t.startswith("grad.") for t in em.tasks]
     remat = ("in", "xf")
     defs = {}
     for i, op in enumerate(em.ops):
         for d in op_dsts(op):
             defs[d] = i
+
+    def is_remat(di):
+        return em.tasks[di] in remat and not (by_task and em.ops[di][0] == "sincos")
+
     exports = {}
     for i, op in enumerate(em.ops):
         if not col[i]:
             continue
         for r in op_srcs(op):
             di = defs[r]
-            if col[di] or em.tasks[di] in remat:
+            if col[di] or is_remat(di):
                 continue
             exports.setdefault(r, len(exports))
+    if by_task:
+        # remat ops feeding exported-by-remat values (transform entries from sin/cos)
+        for i, op in enumerate(em.ops):
+            if em.tasks[i] in remat and op[0] != "sincos":
+                for r in op_srcs(op):
+                    if em.ops[defs[r]][0] == "sincos":
+                        exports.setdefault(r, len(exports))
     pops, ptasks = [], []
     for i, op in enumerate(em.ops):
         if col[i]:
@@ -862,13 +881,29 @@ def split_columns(em):
             if d in exports:
                 pops.append(("xst", exports[d], d))
                 ptasks.append(em.tasks[i])
-    cops = [("imp", r, sl) for r, sl in exports.items()]
-    ctasks = ["imp"] * len(cops)
-    for i, op in enumerate(em.ops):
-        if col[i] or em.tasks[i] in remat:
-            cops.append(op)
-            ctasks.append(em.tasks[i])
-    return _sub_emit(em, pops, ptasks), _sub_emit(em, cops, ctasks), len(exports)
+    imps = [("imp", r, sl) for r, sl in exports.items()]
+    if not by_task:
+        cops = list(imps)
+        ctasks = ["imp"] * len(cops)
+        for i, op in enumerate(em.ops):
+            if col[i] or em.tasks[i] in remat:
+                cops.append(op)
+                ctasks.append(em.tasks[i])
+        return _sub_emit(em, pops, ptasks), _sub_emit(em, cops, ctasks), len(exports)
+    progs = []
+    for task in dict.fromkeys(t for t in em.tasks if t.startswith("grad.")):
+        idx = [i for i, t in enumerate(em.tasks) if t == task]
+        need = {r for i in idx for r in op_srcs(em.ops[i])}
+        keep = set()
+        for i in range(len(em.ops) - 1, -1, -1):  # remat ops this column uses, transitively
+            op = em.ops[i]
+            if em.tasks[i] in remat and op[0] != "sincos" and any(d in need for d in op_dsts(op)):
+                keep.add(i)
+                need |= set(op_srcs(op))
+        cops = list(imps) + [em.ops[i] for i in sorted(keep | set(idx))]
+        ctasks = ["imp"] * len(imps) + [em.tasks[i] for i in sorted(keep | set(idx))]
+        progs.append(_sub_emit(em, cops, ctasks))
+    return _sub_emit(em, pops, ptasks), progs, len(exports)
 
 
 def _lit(x, dtype):
@@ -1412,6 +1447,55 @@ def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=Fal
     return "\n".join(src), em.flops, L
 
 
+def _multi_knot_struct(model, alg, dt, name, progs, nx, over):
+    """One thread-per-knot kernel holding several one-knot programs (the
+    gradient columns of a split program); CTA row blockIdx.y runs program
+    blockIdx.y, so every warp of a CTA streams the same (short) code.  All
+    programs share the register cap and row length of the most demanding."""
+    Ls = [_layout(model, alg, dt, p, over=over) for p in progs]
+    warps = min(L["minb"] * L["bk"] // 32 for L in Ls)
+    over = dict(over, warps_per_sm=warps)
+    Ls = [_layout(model, alg, dt, p, over=over) for p in progs]
+    L0 = dict(Ls[0])
+    L0["sin"] = _odd(max(L["sin"] for L in Ls))
+    L0["minb"] = min(L["minb"] for L in Ls)
+    flops = sum(p.flops for p in progs)
+    head = [
+        f"// GENERATED by paper_2109_06976_b200.codegen -- robot {model.name!r}, {alg} {dt}, "
+        f"{len(progs)} column programs",
+        f"// {flops} flops per knot over all programs; row {L0['sin']} slots, {L0['minb']} CTAs of {L0['bk']} per SM",
+        '#include "rbd_runtime.cuh"',
+    ]
+    bodies, decls = [], []
+    for k, (p, L) in enumerate(zip(progs, Ls)):
+        ctab = ConstTable(f"rbd_c_{name}_{k}", dt)
+        body, sc = ptx_body(p, p.in_total, "global", 0, 0, ctab, L["plan"])
+        if sc:
+            raise GenerationError("column programs import their sin/cos")
+        decls += ctab.declaration()
+        bodies.append((p.tasks[-1], body))
+    src = head + decls + _struct_head(model, alg, dt, L0, flops, name) + [
+        f"  static constexpr int NX = {nx};  // values per knot in the split scratch",
+        f"  static constexpr int NPROG = {len(progs)};",
+        "  __device__ __forceinline__ static void run_dev(T* my, T* o0, T* o1, T* o2, unsigned valid, T* xb) {",
+        "    run_prog(blockIdx.y, my, o0, o1, o2, valid, xb);",
+        "  }",
+        "  __device__ __forceinline__ static void run_prog(int prog, T* my, T* o0, T* o1, T* o2, unsigned valid,",
+        "                                                  T* xb) {",
+        "    const unsigned a_in = (unsigned)__cvta_generic_to_shared(my);",
+        "    switch (prog) {",
+    ]
+    for k, (task, body) in enumerate(bodies):
+        src.append(f"    case {k}:  // {task}")
+        src.append('      asm volatile("{\\n\\t"')
+        for ln in body:
+            src.append(f'        "{ln}\\n\\t"')
+        src.append('        "}" :: "r"(a_in), "l"(o0), "l"(o1), "l"(o2), "r"(valid), "l"(xb) : "memory");')
+        src.append("      break;")
+    src += ["    default: break;", "    }", "  }", "};", ""]
+    return "\n".join(src)
+
+
 def _ws_struct(model, alg, dt, warps, name=None, trees=None, zero_fill=True, fext=False, em=None):
     """Device header of the warp-specialised mapping (see wsched.py).  With
     an `em` holding "imp" ops (split columns), the arena is the per-group
@@ -1536,14 +1620,22 @@ def _big_part_unit(model, alg, dt, tag, K, tn, trees, zero_fill, fx):
     algorithms run warp-specialised as a whole."""
     if alg in ("gradID", "gradFD") and tn.get("split", True):
         em = generate_knot(model, alg, dt, trees, zero_fill, fext=fx, lowmem=True)
-        pre, cols, nx = split_columns(em)
+        by_task = bool(tn.get("split_by_task"))
+        pre, progs, nx = split_columns(em, by_task=by_task)
+        pf = {"park": False, "prefetch_dist": int(tn.get("split_pf_dist", 96)),
+              "prefetch_slack": int(tn.get("split_pf_slack", 12))}
         try:
             ta, _, _ = _knot_struct(model, alg, dt, K + "A", em=pre, nx=nx)
-            # the column kernel writes its n x 2 n outputs per knot as it goes
-            # (parking them would need ~4 KB of row per knot)
-            tb, _, _ = _knot_struct(model, alg, dt, K + "B", em=cols, nx=nx,
-                                    over={"park": False, "prefetch_dist": int(tn.get("split_pf_dist", 96)),
-                                          "prefetch_slack": int(tn.get("split_pf_slack", 12))})
+            if by_task:
+                # one program per gradient column (short code, every warp of a
+                # CTA on the same column); a column whose outputs are all
+                # structural zeros (memset) has no work
+                progs = [p for p in progs if any(op[0] != "st" or not isinstance(op[3], float)
+                                                 for op, t in zip(p.ops, p.tasks) if t.startswith("grad."))]
+                tb = _multi_knot_struct(model, alg, dt, K + "B", progs, nx, pf)
+            else:
+                # all columns in one program; outputs stored as they are produced
+                tb, _, _ = _knot_struct(model, alg, dt, K + "B", em=progs, nx=nx, over=pf)
             return "\n".join([
                 ta.replace("#pragma once\n", ""), tb.replace("#pragma once\n", ""),
                 f'extern "C" int rbd__launch_{alg}_{dt}_{tag}(const void* q, const void* qd, const void* u, '

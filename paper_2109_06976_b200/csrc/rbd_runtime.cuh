@@ -71,6 +71,17 @@ struct rbd_park_traits<K, decltype((void)K::NOUT, void())> {
   static constexpr int nout = K::NOUT;
   static constexpr bool ofull = K::OFULL;
 };
+template <class K, class = void>
+struct rbd_prog_traits {
+  static constexpr int nprog = 1;
+};
+template <class K>
+struct rbd_prog_traits<K, decltype((void)K::NPROG, void())> {
+  static constexpr int nprog = K::NPROG;
+};
+template <class K>
+__host__ __device__ constexpr int rbd_nprog() { return rbd_prog_traits<K>::nprog; }
+
 template <class K>
 __host__ __device__ constexpr int rbd_nout() { return rbd_park_traits<K>::nout; }
 template <class K>
@@ -367,7 +378,8 @@ static int rbd_launch_kernel(const void* q, const void* qd, const void* u, const
   } else {
     const long long grid = (N + K::BK - 1) / K::BK;
     if (K::NX && !xs) return RBD_EINVAL;
-    rbd_batch_kernel<K><<<(unsigned)grid, K::BK, smem, (cudaStream_t)stream>>>(
+    // several programs (split gradient columns): grid row y runs program y
+    rbd_batch_kernel<K><<<dim3((unsigned)grid, rbd_nprog<K>()), K::BK, smem, (cudaStream_t)stream>>>(
         (const T*)q, (const T*)qd, (const T*)u, (const T*)fx, (T*)o0, (T*)o1, (T*)o2, (long long)N,
         (T*)xs);
   }

@@ -282,6 +282,32 @@ def test_split_prefix_and_columns(name, trees, alg):
     touts = [dict(o) for o in outs]
     ptxsim.run_block(lines, [crow] + touts + [None, dict(scratch)], [8, 8, 8, 8, 8, 32 * 8],
                      consts={"K": sorted(ctab.index, key=ctab.index.get)})
+    # one program per gradient column (the product kernel's layout): sin/cos
+    # exported too, each program reading only what it uses
+    pre2, progs, nx2 = codegen.split_columns(em, by_task=True)
+    ctab = codegen.ConstTable("K", "f64")
+    lines, sc = codegen.ptx_body(pre2, pre2.in_total, "global", ctab=ctab,
+                                 plan=codegen.SpillPlan(pre2, 48, codegen.row_homes(pre2, pre2.in_total),
+                                                        pre2.in_total + 2 * len(_sincos_slots(pre2)),
+                                                        park_outputs=True))
+    row2 = {i: float(v) for i, v in enumerate(x)}
+    for j, slot in enumerate(sc):
+        row2[pre2.in_total + 2 * j] = math.sin(x[slot])
+        row2[pre2.in_total + 2 * j + 1] = math.cos(x[slot])
+    scratch2 = {}
+    ptxsim.run_block(lines, [row2, {}, {}, {}, None, scratch2], [8, 8, 8, 8, 8, 32 * 8],
+                     consts={"K": sorted(ctab.index, key=ctab.index.get)})
+    assert len(scratch2) == nx2
+    pouts = [dict(o) for o in outs]
+    for prog in progs:
+        assert not any(op[0] == "sincos" for op in prog.ops)
+        cp = codegen.SpillPlan(prog, 24, codegen.row_homes(prog, prog.in_total), prog.in_total, prefetch=(32, 4))
+        ctab = codegen.ConstTable("K", "f64")
+        lines, _ = codegen.ptx_body(prog, prog.in_total, "global", ctab=ctab, plan=cp)
+        prow = {i: float(v) for i, v in enumerate(x)}
+        ptxsim.run_block(lines, [prow] + pouts + [None, dict(scratch2)], [8, 8, 8, 8, 8, 32 * 8],
+                         consts={"K": sorted(ctab.index, key=ctab.index.get)})
+    touts = [touts, pouts]
     # columns: one phase, arena = the scratch
     P = wsched.plan(m, alg, "f64", 6, em=cols)
     S = P["sched"]
@@ -298,7 +324,7 @@ def test_split_prefix_and_columns(name, trees, alg):
             ptxsim.run_block(lines, [srow, scratch] + outs + [None], [L * 8, 32 * 8, 8, 8, 8],
                              consts={"K": sorted(ctab.index, key=ctab.index.get)})
     owned = set(range(lo, lo + np_))
-    for variant in (outs, touts):
+    for variant in [outs] + touts:
         for (nm, e), o in zip(codegen.outputs(alg, n), variant):
             ref = g[f"{alg}.{nm}"][k]
             idx = [i for i in range(e) if (i // n in owned and i % n in owned) if e == n * n] or \
