@@ -770,7 +770,9 @@ for _a in ALGORITHMS:
                                          "zero_memset": True, "split": True,
                                          # measured at N = 2^18: per-column programs win in fp32
                                          # (4.6 -> 4.3 ms), lose in fp64 (7.6 -> 8.4 ms)
-                                         "split_by_task": _d == "f32"}
+                                         "split_by_task": _d == "f32",
+                                         # knots per split launch pair (measured: fp64 32768, fp32 24576)
+                                         "split_chunk": 32768 if _d == "f64" else 24576}
 
 
 def tuning(model=None, alg=None, dtype=None):
@@ -1626,6 +1628,12 @@ def _big_part_unit(model, alg, dt, tag, K, tn, trees, zero_fill, fx):
               "prefetch_slack": int(tn.get("split_pf_slack", 12))}
         try:
             ta, _, _ = _knot_struct(model, alg, dt, K + "A", em=pre, nx=nx)
+            # knots per launch pair: large enough that the prefix kernel fills
+            # the GPU, small enough that the scratch mostly stays in L2
+            chunk = int(tn.get("split_chunk") or 32768)
+            ta = ta.replace(f"  static constexpr int NX = {nx};",
+                            f"  static constexpr int NX = {nx};\n  static constexpr int CHUNK = {chunk};"
+                            "  // knots per split launch pair")
             if by_task:
                 # one program per gradient column (short code, every warp of a
                 # CTA on the same column); a column whose outputs are all

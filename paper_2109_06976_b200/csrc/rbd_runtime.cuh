@@ -389,30 +389,29 @@ static int rbd_launch_kernel(const void* q, const void* qd, const void* u, const
 // ---------------------------------------------------------------------------
 // split gradient program (large root trees): the prefix kernel KA (thread per
 // knot: RNEA, articulated inertias, Minv, FD, RNEA at qdd) exports the values
-// the gradient columns need to a scratch; the column kernel KB (warp-
-// specialised, one phase, no barriers between columns) reads them as its
-// arena.  Chunks of RBD_SPLIT_CHUNK knots keep the scratch L2-resident.
+// the gradient columns need to a scratch; the column kernel KB (thread per
+// knot) reloads them through its register plan.  Chunks of KA::CHUNK knots
+// keep the scratch L2-resident.
 // ---------------------------------------------------------------------------
-#define RBD_SPLIT_CHUNK 32768
 template <class KA, class KB>
 static int rbd_launch_split(const void* q, const void* qd, const void* u, const void* fx, void* o0,
                             void* o1, void* o2, int64_t N, void* stream) {
   typedef typename KA::T T;
   static_assert(KA::NX == KB::NX && KA::MAP == 0 && KB::MAP == 0, "prefix exports and column imports disagree");
-  static_assert(RBD_SPLIT_CHUNK % KA::BK == 0 && KA::BK % 32 == 0, "chunk / CTA / warp alignment");
+  static_assert(KA::CHUNK % KA::BK == 0 && KA::BK % 32 == 0, "chunk / CTA / warp alignment");
   if (N < 0) return RBD_EINVAL;
   if (N == 0) return 0;
   static void* scratch[64] = {nullptr};
   int dev = 0;
   cudaGetDevice(&dev);
   if (!scratch[dev & 63]) {
-    cudaError_t e = cudaMalloc(&scratch[dev & 63], sizeof(T) * (size_t)RBD_SPLIT_CHUNK * KA::NX);
+    cudaError_t e = cudaMalloc(&scratch[dev & 63], sizeof(T) * (size_t)KA::CHUNK * KA::NX);
     if (e != cudaSuccess) return (int)e;
   }
   void* xs = scratch[dev & 63];
   constexpr int n = KA::NDOF;
-  for (int64_t c0 = 0; c0 < N; c0 += RBD_SPLIT_CHUNK) {
-    const int64_t nk = (N - c0) < RBD_SPLIT_CHUNK ? (N - c0) : RBD_SPLIT_CHUNK;
+  for (int64_t c0 = 0; c0 < N; c0 += KA::CHUNK) {
+    const int64_t nk = (N - c0) < KA::CHUNK ? (N - c0) : KA::CHUNK;
     const T* cq = (const T*)q + c0 * n;
     const T* cqd = qd ? (const T*)qd + c0 * n : nullptr;
     const T* cu = u ? (const T*)u + c0 * n : nullptr;
