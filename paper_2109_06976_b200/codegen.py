@@ -772,7 +772,9 @@ for _a in ALGORITHMS:
                                          # (4.6 -> 4.3 ms), lose in fp64 (7.6 -> 8.4 ms)
                                          "split_by_task": _d == "f32",
                                          # knots per split launch pair (measured: fp64 32768, fp32 24576)
-                                         "split_chunk": 32768 if _d == "f64" else 24576}
+                                         "split_chunk": 32768 if _d == "f64" else 24576,
+                                         # column-kernel register budget (fp64: 80 + 12 prefetch beat 107 + 12)
+                                         "split_budget": 80 if _d == "f64" else 0}
 
 
 def tuning(model=None, alg=None, dtype=None):
@@ -1625,7 +1627,7 @@ def _big_part_unit(model, alg, dt, tag, K, tn, trees, zero_fill, fx):
         by_task = bool(tn.get("split_by_task"))
         pre, progs, nx = split_columns(em, by_task=by_task)
         pf = {"park": False, "prefetch_dist": int(tn.get("split_pf_dist", 96)),
-              "prefetch_slack": int(tn.get("split_pf_slack", 12))}
+              "prefetch_slack": int(tn.get("split_pf_slack", 12)), "ra_budget": int(tn.get("split_budget", 0))}
         try:
             ta, _, _ = _knot_struct(model, alg, dt, K + "A", em=pre, nx=nx)
             # knots per launch pair: large enough that the prefix kernel fills
