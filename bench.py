@@ -410,6 +410,28 @@ def sweep(torch, stream, args):
     entry("quad12", "gradFD", "f32", 128)
     entry("humanoid30", "gradFD", "f64", 256)
     entry("humanoid30", "gradFD", "f32", 256)
+    # device-resident rollouts (rollout.py): B trajectories x H steps of gradFD + Euler, graph-replayed
+    from paper_2109_06976_b200.rollout import Rollout
+    for robot, B, H in (("chain7", 128, 64), ("chain7", 4096, 64), ("humanoid30", 128, 32)):
+        m = models.load(robot)
+        n = m.n_dof
+        r = Rollout(m, B, H, 0.01, "f64", grad=True, graph=True)
+        rng = np.random.default_rng(1)
+        q0 = torch.from_numpy(rng.uniform(-1, 1, (B, n))).cuda()
+        tau = torch.from_numpy(rng.uniform(-1, 1, (B, H, n))).cuda()
+        for _ in range(3):
+            r.run(q0, q0, tau)
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(10):
+            r.run(q0, q0, tau)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 10
+        out.append({"robot": robot, "paper_robot": PAPER.get(robot), "alg": "rollout(gradFD+Euler)", "dtype": "f64",
+                    "N": B * H, "trajectories": B, "horizon": H, "kernel_us": ms * 1e3,
+                    "kernel_knots_per_s": B * H / (ms * 1e-3), "graph": True})
     for robot in ("chain7", "quad12", "humanoid30"):
         for dt in ("f64", "f32"):
             Ns = {"chain7": (65536, 262144, 1048576), "quad12": (1048576,), "humanoid30": (65536, 262144)}[robot]

@@ -148,6 +148,12 @@ int rbd_run_host_fext(rbd_session* s, int alg, int dtype, const void* q, const v
                       const void* u, const void* f_ext, void* out0, void* out1, void* out2,
                       int64_t N);
 
+/* Device-resident rollouts (the paper's trajectory-optimisation use case):
+ * one semi-implicit Euler step for N knots of this robot, device pointers,
+ * [N][n] arrays: qd_next = qd + dt * qdd, q_next = q + dt * qd_next. */
+int rbd_euler_step(int dtype, const void* q, const void* qd, const void* qdd, void* q_next,
+                   void* qd_next, int64_t N, double dt, void* stream);
+
 /* Benchmark helper (not in the reference interface): calls rbd_run_host
  * `reps` times back to back and stores the mean host wall time per call in
  * *seconds (steady clock) -- the end-to-end latency a C/C++ caller sees,

@@ -674,6 +674,39 @@ extern "C" int rbd_run_host_fext(rbd_session* s, int alg, int dtype, const void*
   return rbd_run_host_impl(s, alg, dtype, q, qd, u, f_ext, out0, out1, out2, N);
 }
 
+// ---------------------------------------------------------------------------
+// semi-implicit Euler step of a batch of trajectories (device-resident rollouts)
+//   qd' = qd + dt * qdd ;  q' = q + dt * qd'
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void rbd_euler_kernel(const T* __restrict__ q, const T* __restrict__ qd,
+                                 const T* __restrict__ qdd, T* __restrict__ q1, T* __restrict__ qd1,
+                                 long long count, T dt) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    const T v = fma(dt, qdd[i], qd[i]);
+    qd1[i] = v;
+    q1[i] = fma(dt, v, q[i]);
+  }
+}
+
+extern "C" int rbd_euler_step(int dtype, const void* q, const void* qd, const void* qdd, void* q_next,
+                              void* qd_next, int64_t N, double dt, void* stream) {
+  if (N < 0 || !q || !qd || !qdd || !q_next || !qd_next) return RBD_EINVAL;
+  if (N == 0) return 0;
+  const long long count = (long long)N * rbd_ndof();
+  const unsigned grid = (unsigned)((count + 255) / 256 < 4096 ? (count + 255) / 256 : 4096);
+  if (dtype == RBD_F64)
+    rbd_euler_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>(
+        (const double*)q, (const double*)qd, (const double*)qdd, (double*)q_next, (double*)qd_next, count, dt);
+  else if (dtype == RBD_F32)
+    rbd_euler_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>(
+        (const float*)q, (const float*)qd, (const float*)qdd, (float*)q_next, (float*)qd_next, count, (float)dt);
+  else
+    return RBD_EINVAL;
+  return (int)cudaGetLastError();
+}
+
 extern "C" int rbd_bench_host(rbd_session* s, int alg, int dtype, const void* q, const void* qd,
                               const void* u, void* out0, void* out1, void* out2, int64_t N,
                               int32_t reps, double* seconds) {

@@ -142,7 +142,8 @@ class RbdInfo(ctypes.Structure):
 
 
 ABI_SYMBOLS = (["rbd_get_info", "rbd_alg_extents", "rbd_launch", "rbd_launch_fext", "rbd_session_create",
-                "rbd_session_destroy", "rbd_run_host", "rbd_run_host_fext", "rbd_bench_host"]
+                "rbd_session_destroy", "rbd_run_host", "rbd_run_host_fext", "rbd_bench_host",
+                "rbd_euler_step"]
                + [f"rbd_{a}_{d}" for a in codegen.ALGORITHMS for d in codegen.DTYPES]
                + [f"rbd_{a}_{d}_fext" for a in codegen.FEXT_ALGORITHMS for d in codegen.DTYPES])
 
@@ -154,6 +155,7 @@ def _bind(lib):
     lib.rbd_alg_extents.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int32)] + [ctypes.POINTER(ctypes.c_int64)] * 3
     lib.rbd_launch.argtypes = [ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp]
     lib.rbd_launch_fext.argtypes = [ctypes.c_int, ctypes.c_int] + [_vp] * 7 + [ctypes.c_int64, _vp]
+    lib.rbd_euler_step.argtypes = [ctypes.c_int] + [_vp] * 5 + [ctypes.c_int64, ctypes.c_double, _vp]
     lib.rbd_run_host_fext.argtypes = [_vp, ctypes.c_int, ctypes.c_int] + [_vp] * 7 + [ctypes.c_int64]
     lib.rbd_session_create.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(_vp)]
     lib.rbd_session_destroy.argtypes = [_vp]
