@@ -238,8 +238,12 @@ def cmd_report(csv_path, out_dir):
 # ---------------------------------------------------------------------------
 
 def cmd_dump_kernel(args):
-    """The generated CUDA translation unit(s) of one (robot, algorithm, dtype)."""
+    """The generated CUDA translation unit(s) of one (robot, algorithm, dtype),
+    or (--format rbdkernel) the program in the reference's kernel text format."""
     m = _load_model(args)
+    if getattr(args, "format", "cuda") == "rbdkernel":
+        from . import kdump
+        return kdump.dump_text(m, args.alg, args.dtype)
     files, _ = codegen.generate_sources(m, algorithms=(args.alg,), dtypes=(args.dtype,))
     return "\n".join(f"// ===== {nm}\n{txt}" for nm, txt in sorted(files.items()) if nm != "main.cu")
 
@@ -292,6 +296,7 @@ def main(argv=None):
     p.add_argument("--out", default="report")
     p = sub.add_parser("dump-kernel")
     common(p)
+    p.add_argument("--format", choices=("cuda", "rbdkernel"), default="cuda")
     p = sub.add_parser("dump-schedule")
     common(p)
     p.add_argument("--warps", type=int, default=8)

@@ -87,5 +87,19 @@ def main():
         print(name, n, os.path.getsize(path))
 
 
+def kernel_dumps():
+    """The reference's own generated programs as "rbdkernel v1" text
+    (ir.py:161), written exactly as its dump_text emits them (numpy >= 2
+    constants included: `np.float64(...)`)."""
+    from rbdgen import codegen, ir
+    for name, alg in (("chain7", "gradFD"), ("quad12", "gradID"), ("tree7", "FD"), ("mixed5", "Minv")):
+        prog = codegen.build(models.load(name), alg)[0]
+        path = os.path.join(HERE, f"rbdkernel_{name}_{alg}.txt")
+        with open(path, "w") as fh:
+            fh.write(ir.dump_text(prog))
+        print(path, os.path.getsize(path))
+
+
 if __name__ == "__main__":
     main()
+    kernel_dumps()

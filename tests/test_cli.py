@@ -49,6 +49,9 @@ def test_dumps_without_gpu(capsys):
     assert cli.main(["dump-kernel", "--model", "pendulum2", "--alg", "ID", "--dtype", "f64"]) == 0
     out = capsys.readouterr().out
     assert "rbd__launch_ID_f64_T" in out and "fma.rn.f64" in out
+    assert cli.main(["dump-kernel", "--model", "pendulum2", "--alg", "ID", "--format", "rbdkernel"]) == 0
+    out = capsys.readouterr().out
+    assert out.startswith("rbdkernel v1") and "output tau_out" in out
 
 
 @pytest.mark.gpu
