@@ -343,7 +343,9 @@ def run_ours(args):
                    "l2": "inputs+outputs per step exceed the 126 MB L2 (no flush needed)"},
         "e2e": {"value": e2e, "unit": "knots/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_s * 1e3, "path": "Python Session.run -> rbd_run_host (C ABI, pinned host buffers)",
-                "c_abi_ms_per_step": e2e_c * 1e3},
+                "c_abi_ms_per_step": e2e_c * 1e3,
+                # PCIe-bound: host<->device bytes per step over the step time
+                "io_gbs": (h2d + d2h) / e2e_s / 1e9},
         "roofline": {"bound": "fp64" if dt == "f64" else "fp32", "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
                      "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes": alg_bytes,

@@ -1,5 +1,5 @@
-VARIANTS=tools/variants_c7.txt bash tools/variants.sh time chain7 gradFD f64 1048576 2>&1 | python -c "
+for dt in f64 f32; do VARIANTS=tools/variants_c7.txt bash tools/variants.sh time chain7 gradFD $dt 1048576 2>&1 | python -c "
 import sys, json
 for l in sys.stdin:
     try: d=json.loads(l); print(d['dtype'], d['tuning'], round(d['us'],1), '%.3g'%d['knots_per_s'])
-    except Exception: print(l[:200])"
+    except Exception: print(l[:200])"; done
