@@ -1653,6 +1653,14 @@ def _big_part_unit(model, alg, dt, tag, K, tn, trees, zero_fill, fx):
                 "                                void* o0, void* o1, void* o2, int64_t N, void* stream) {",
                 f"  return rbd_launch_split<{K}A, {K}B>(q, qd, u, fx, o0, o1, o2, N, stream);",
                 "}",
+                f'extern "C" int rbd__fork_{alg}_{dt}_{tag}(const void* q, const void* qd, const void* u, '
+                "const void* fx,",
+                "                                void* o0, void* o1, void* o2, int64_t N, void* stream) {",
+                f"  return rbd_launch_split<{K}A, {K}B>(q, qd, u, fx, o0, o1, o2, N, stream, false);",
+                "}",
+                f'extern "C" int rbd__join_{alg}_{dt}_{tag}(void* stream) {{',
+                f"  return rbd_split_join<{K}A, {K}B>(stream);",
+                "}",
                 "",
             ])
         except GenerationError:
@@ -1705,7 +1713,7 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
                 # structural zeros by a coalesced memset ("zero_memset") or by part 0
                 parts = tn.get("parts") or []
                 zf = not tn.get("zero_memset")
-                ptags = []
+                ptags, split_tags = [], []
                 for pi, trees in enumerate(parts):
                     tag = f"P{pi}{X}"
                     K = f"Knot_{alg}_{dt}_{tag}"
@@ -1719,11 +1727,22 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
                     except GenerationError:
                         files[f"k_{alg}_{dt}_{tag}.cu"] = _big_part_unit(model, alg, dt, tag, K, tn, tuple(trees),
                                                                          zf and pi == 0, fx)
+                        if "rbd__fork_" in files[f"k_{alg}_{dt}_{tag}.cu"]:
+                            split_tags.append(tag)
                     ptags.append(tag)
                 for tag in tags + ptags:
                     dispatch.append(f'extern "C" int rbd__launch_{alg}_{dt}_{tag}{sig}')
+                for tag in split_tags:
+                    dispatch.append(f'extern "C" int rbd__fork_{alg}_{dt}_{tag}{sig}')
+                    dispatch.append(f'extern "C" int rbd__join_{alg}_{dt}_{tag}(void*);')
                 if ptags:
-                    seq = " ".join(f"if ((rc = rbd__launch_{alg}_{dt}_{t}{args}) != 0) return rc;" for t in ptags)
+                    # split parts run their pipeline on side streams while the
+                    # other parts (independent root trees) run on the caller's
+                    seq = " ".join([f"if ((rc = rbd__fork_{alg}_{dt}_{t}{args}) != 0) return rc;" for t in split_tags]
+                                   + [f"if ((rc = rbd__launch_{alg}_{dt}_{t}{args}) != 0) return rc;"
+                                      for t in ptags if t not in split_tags]
+                                   + [f"if ((rc = rbd__join_{alg}_{dt}_{t}(stream)) != 0) return rc;"
+                                      for t in split_tags])
                     zs = ""
                     if not zf and alg in ("Minv", "gradID", "gradFD"):
                         es = 8 if dt == "f64" else 4

@@ -22,6 +22,7 @@
 #include <math.h>
 #if defined(__CUDACC__)
 #include <chrono>
+#include <mutex>
 #endif
 
 #include "rbd_b200.h"
@@ -393,24 +394,82 @@ static int rbd_launch_kernel(const void* q, const void* qd, const void* u, const
 // knot) reloads them through its register plan.  Chunks of KA::CHUNK knots
 // keep the scratch L2-resident.
 // ---------------------------------------------------------------------------
+// Per-device side streams and events of the split pipeline (created once).
+struct rbd_split_state {
+  bool init = false;
+  void* scratch[2] = {nullptr, nullptr};
+  size_t bytes = 0;
+  cudaStream_t sa = nullptr, sb = nullptr;
+  cudaEvent_t start = nullptr, done_a[2] = {nullptr, nullptr}, done_b[2] = {nullptr, nullptr};
+};
+
+template <class KA, class KB>
+static rbd_split_state& rbd_split_state_of(int dev) {
+  static rbd_split_state state[64];
+  return state[dev & 63];
+}
+
+// Join: the caller's stream continues after both side streams of the split
+// pipeline on the current device.
+template <class KA, class KB>
+static int rbd_split_join(void* stream) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  rbd_split_state& st = rbd_split_state_of<KA, KB>(dev);
+  if (!st.init) return 0;
+  cudaStream_t s0 = (cudaStream_t)stream;
+  cudaError_t e;
+  if ((e = cudaEventRecord(st.done_a[0], st.sa)) != cudaSuccess) return (int)e;
+  if ((e = cudaStreamWaitEvent(s0, st.done_a[0], 0)) != cudaSuccess) return (int)e;
+  if ((e = cudaEventRecord(st.done_b[0], st.sb)) != cudaSuccess) return (int)e;
+  if ((e = cudaStreamWaitEvent(s0, st.done_b[0], 0)) != cudaSuccess) return (int)e;
+  return 0;
+}
+
+// Fork: enqueue the whole split pipeline on the side streams (after the work
+// already on the caller's stream) and return without joining, so the caller
+// can enqueue independent work (other root trees) meanwhile.  join = true:
+// also join before returning.
 template <class KA, class KB>
 static int rbd_launch_split(const void* q, const void* qd, const void* u, const void* fx, void* o0,
-                            void* o1, void* o2, int64_t N, void* stream) {
+                            void* o1, void* o2, int64_t N, void* stream, bool join = true) {
   typedef typename KA::T T;
   static_assert(KA::NX == KB::NX && KA::MAP == 0 && KB::MAP == 0, "prefix exports and column imports disagree");
   static_assert(KA::CHUNK % KA::BK == 0 && KA::BK % 32 == 0, "chunk / CTA / warp alignment");
   if (N < 0) return RBD_EINVAL;
   if (N == 0) return 0;
-  static void* scratch[64] = {nullptr};
+  static std::mutex lock;  // host side: the shared events / side streams of one device
+  std::lock_guard<std::mutex> guard(lock);
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!scratch[dev & 63]) {
-    cudaError_t e = cudaMalloc(&scratch[dev & 63], sizeof(T) * (size_t)KA::CHUNK * KA::NX);
+  rbd_split_state& st = rbd_split_state_of<KA, KB>(dev);
+  const size_t bytes = sizeof(T) * (size_t)KA::CHUNK * KA::NX;
+  if (!st.init) {
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaMalloc(&st.scratch[i], bytes);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st.sa, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st.sb, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&st.start, cudaEventDisableTiming);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+      e = cudaEventCreateWithFlags(&st.done_a[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&st.done_b[i], cudaEventDisableTiming);
+    }
     if (e != cudaSuccess) return (int)e;
+    st.bytes = bytes;
+    st.init = true;
   }
-  void* xs = scratch[dev & 63];
+  if (st.bytes < bytes) return RBD_EINVAL;  // one split kernel pair per (device, scratch size) class
+  // pipeline over two scratch buffers: prefix(i+1) on stream A overlaps
+  // columns(i) on stream B; A reuses buffer b only after B has read it
+  cudaStream_t s0 = (cudaStream_t)stream;
+  cudaError_t e = cudaEventRecord(st.start, s0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st.sa, st.start, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st.sb, st.start, 0);
+  if (e != cudaSuccess) return (int)e;
   constexpr int n = KA::NDOF;
-  for (int64_t c0 = 0; c0 < N; c0 += KA::CHUNK) {
+  int chunk = 0;
+  for (int64_t c0 = 0; c0 < N; c0 += KA::CHUNK, ++chunk) {
+    const int buf = chunk & 1;
     const int64_t nk = (N - c0) < KA::CHUNK ? (N - c0) : KA::CHUNK;
     const T* cq = (const T*)q + c0 * n;
     const T* cqd = qd ? (const T*)qd + c0 * n : nullptr;
@@ -419,12 +478,16 @@ static int rbd_launch_split(const void* q, const void* qd, const void* u, const 
     T* c_o0 = (T*)o0 + c0 * KA::E0;
     T* c_o1 = KA::E1 ? (T*)o1 + c0 * KA::E1 : nullptr;
     T* c_o2 = KA::E2 ? (T*)o2 + c0 * KA::E2 : nullptr;
-    int rc = rbd_launch_kernel<KA>(cq, cqd, cu, cfx, c_o0, c_o1, c_o2, nk, stream, xs);
+    if (chunk >= 2 && (e = cudaStreamWaitEvent(st.sa, st.done_b[buf], 0)) != cudaSuccess) return (int)e;
+    int rc = rbd_launch_kernel<KA>(cq, cqd, cu, cfx, c_o0, c_o1, c_o2, nk, (void*)st.sa, st.scratch[buf]);
     if (rc) return rc;
-    rc = rbd_launch_kernel<KB>(cq, cqd, cu, cfx, c_o0, c_o1, c_o2, nk, stream, xs);
+    if ((e = cudaEventRecord(st.done_a[buf], st.sa)) != cudaSuccess) return (int)e;
+    if ((e = cudaStreamWaitEvent(st.sb, st.done_a[buf], 0)) != cudaSuccess) return (int)e;
+    rc = rbd_launch_kernel<KB>(cq, cqd, cu, cfx, c_o0, c_o1, c_o2, nk, (void*)st.sb, st.scratch[buf]);
     if (rc) return rc;
+    if ((e = cudaEventRecord(st.done_b[buf], st.sb)) != cudaSuccess) return (int)e;
   }
-  return 0;
+  return join ? rbd_split_join<KA, KB>(stream) : 0;
 }
 
 // ---------------------------------------------------------------------------
