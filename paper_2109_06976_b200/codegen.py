@@ -756,7 +756,10 @@ TUNING_DEFAULT = {
 TUNED = {}
 # measured on B200 (N = 2^20): chain7 gradFD fp64 is compute-bound at 6 warps/SM
 # either way; per-thread output stores beat parking there (1.35 vs 1.43 ms)
-TUNED[("chain7", "gradFD", "f64")] = {"park": False}
+TUNED[("chain7", "gradFD", "f64")] = {"park": False, "bk": 32}
+# 32-knot CTAs: finer-grained CTA turnover (staging / write-back barriers),
+# measured 1.35 -> 1.22 ms (fp64) and 0.64 -> 0.60 ms (fp32) at N = 2^20
+TUNED[("chain7", "gradFD", "f32")] = {"bk": 32}
 for _a in ALGORITHMS:
     for _d in DTYPES:
         # measured on B200: with outputs parked in the row, quad12's

@@ -1,6 +1,5 @@
-RBD_TUNING='{}' timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "humanoid30 and large" 2>&1 | tail -1
-for dt in f64 f32; do VARIANTS=tools/variants_h30.txt bash tools/variants.sh time humanoid30 gradFD $dt 262144 2>&1 | python -c "
+for dt in f32 f64; do VARIANTS=tools/variants_c7.txt bash tools/variants.sh time chain7 gradFD $dt 1048576 262144 2>&1 | python -c "
 import sys, json
 for l in sys.stdin:
-    try: d=json.loads(l); print(d['dtype'], d['tuning'], round(d['us'],1), '%.3g'%d['knots_per_s'])
+    try: d=json.loads(l); print(d['dtype'], d['N'], d['tuning'], round(d['us'],1), '%.3g'%d['knots_per_s'])
     except Exception: print(l[:200])"; done
