@@ -739,7 +739,9 @@ def _odd(x):
 # TUNED once measured.
 TUNING_DEFAULT = {
     "maps": ["thread", "ws"],  # kernels compiled; launch picks ws for N <= ws_max_n
-    "ws_max_n": 16384,   # batch size up to which the (lower-latency) warp-specialised kernel runs
+    "ws_max_n": 8192,    # batch size up to which the (lower-latency) warp-specialised kernel runs
+                         # (measured crossover for chain7: ws 20.6 vs thread 28.8 us at 8192,
+                         # thread ahead at 16384)
     "warps": 8,          # ws: warps per CTA (one 32-knot group per CTA)
     "minb": 2,           # ws: min CTAs per SM (caps registers at 64K / (32 W minb))
     "bk": 64,            # thread: knots (threads) per CTA
@@ -766,10 +768,11 @@ for _a in ALGORITHMS:
         # thread-per-knot kernel runs at ~80% of HBM bandwidth at N = 2^20
         # (3.4x the warp-specialised one); humanoid30's one-knot program
         # (~600 live values) does not fit a thread
-        TUNED[("quad12", _a, _d)] = {"warps": 16, "minb": 1}
+        TUNED[("quad12", _a, _d)] = {"warps": 16, "minb": 1, "ws_max_n": 4096}  # thread ahead from 8192
         # humanoid30: small batches on the warp-specialised kernel; large ones
         # per root tree (torso tree, two legs)
         TUNED[("humanoid30", _a, _d)] = {"maps": ["ws"], "warps": 16, "minb": 1, "parts": [[0], [1], [2]],
+                                         "ws_max_n": 4096,  # measured: parts ahead from 8192 knots
                                          "zero_memset": True, "split": True,
                                          # measured at N = 2^18: per-column programs win in fp32
                                          # (4.6 -> 4.3 ms), lose in fp64 (7.6 -> 8.4 ms)
