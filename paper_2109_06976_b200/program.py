@@ -72,14 +72,20 @@ def build(model, algorithm, budget=None):
     except OSError:
         flops = {}
     bk = codegen.knots_per_block(model, algorithm, "f64")
-    ext = sum(e for _, e in codegen.outputs(algorithm, n))
-    nin = len(codegen.INPUTS[algorithm])
 
-    def smem(es):
-        stage = codegen.stage_outputs(model, algorithm, "f64" if es == 8 else "f32", bk)
-        return bk * es * (codegen._odd(nin * n) + (codegen._odd(ext) if stage else 0))
+    def smem(dt):
+        """Shared memory per CTA of the large-batch thread-per-knot kernel
+        (knot rows incl. the register plan's parked values); None when the
+        robot's large batches run as per-tree parts / split programs."""
+        if codegen.tuning(model, algorithm, dt).get("parts"):
+            return None
+        try:
+            L = codegen._layout(model, algorithm, dt, codegen.generate_knot(model, algorithm, dt))
+        except codegen.GenerationError:
+            return None
+        return L["bk"] * L["sin"] * (8 if dt == "f64" else 4)
 
-    layout = KernelLayout(model.name, algorithm, bk, smem(8), smem(4), budget)
+    layout = KernelLayout(model.name, algorithm, bk, smem("f64"), smem("f32"), budget)
     prog = CudaProgram(model, algorithm, ins, outs, meta, flops)
     prog._lib = lib
     return prog, build_levels(model), layout
