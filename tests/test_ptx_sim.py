@@ -195,8 +195,8 @@ def test_spill_plan_invariants():
     for i, op in enumerate(em.ops):
         for r in codegen.op_srcs(op):
             last[r] = i
-    for budget in (8, 40, 119):
-        plan = codegen.SpillPlan(em, budget, homes, 35, park_outputs=True)
+    for budget, pf in ((8, None), (40, None), (119, None), (24, (32, 4)), (96, (96, 12))):
+        plan = codegen.SpillPlan(em, budget, homes, 35, park_outputs=True, prefetch=pf)
         owner = {sl: v for v, sl in homes.items()}
         for i, op in enumerate(em.ops):
             for a in plan.before.get(i, ()):

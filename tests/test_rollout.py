@@ -55,3 +55,24 @@ def test_rollout_without_gradients_and_shape_errors():
     assert np.allclose(qdd[0, 0].cpu().numpy(), ref, rtol=1e-12, atol=1e-12)
     with pytest.raises(ValueError):
         rollout(m, q0, q0, tau[:, :, :5], 0.005)
+
+
+def test_rollout_fp32():
+    from paper_2109_06976_b200.rollout import Rollout
+    m = models.load("chain7")
+    n, B, H, dt = m.n_dof, 8, 5, 0.01
+    rng = np.random.default_rng(5)
+    q0, qd0 = rng.uniform(-1, 1, (B, n)).astype(np.float32), rng.uniform(-1, 1, (B, n)).astype(np.float32)
+    tau = rng.uniform(-1, 1, (B, H, n)).astype(np.float32)
+    r = Rollout(m, B, H, dt, "f32", grad=False, graph=True)
+    r.run(torch.from_numpy(q0).cuda(), torch.from_numpy(qd0).cuda(), torch.from_numpy(tau).cuda())
+    torch.cuda.synchronize()
+    q, qd, qdd = (x.cpu().numpy().astype(np.float64) for x in r.trajectories())
+    for b in range(B):
+        qb, qdb = q0[b].astype(np.float64), qd0[b].astype(np.float64)
+        for k in range(H):
+            ref = R.forward_dynamics(m, qb, qdb, tau[b, k].astype(np.float64))
+            assert rel_err(qdd[b, k][None], ref[None]) < 1e-3  # fp32 kernels along an fp64 reference path
+            qdb = qdb + dt * ref
+            qb = qb + dt * qdb
+        assert rel_err(q[b, H][None], qb[None]) < 1e-4
