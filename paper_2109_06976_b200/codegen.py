@@ -205,33 +205,34 @@ class _Emit:
         if not prods and len(sing) == 1 and const == 0.0:
             return Var(sing[0][0], sing[0][1])
         acc = const if const != 0.0 else None
+        if acc is None:
+            # start the sum from a +-1-scaled single: it becomes the first
+            # FMA's addend (no separate multiply or final add; a negation
+            # folds into the DFMA operand)
+            for idx, (nm, c) in enumerate(sing):
+                if c in (1.0, -1.0):
+                    acc = nm if c == 1.0 else self.op("neg", nm)
+                    sing = sing[:idx] + sing[idx + 1:]
+                    break
+        for nm, c in sing:
+            if acc is None:
+                acc = self.op("mul", nm, c) if c not in (1.0, -1.0) else (nm if c == 1.0 else self.op("neg", nm))
+            elif c == 1.0:
+                acc = self.op("add", nm, acc) if isinstance(acc, float) else self.op("add", acc, nm)
+            elif c == -1.0:
+                acc = self.op("add", self.op("neg", nm), acc) if isinstance(acc, float) else self.op("sub", acc, nm)
+            else:
+                acc = self.op("fma", nm, c, acc)
         for c, a, b in prods:
             if c == -1.0:
                 a = self.op("neg", a)
             elif c != 1.0:
                 a = self.op("mul", a, c)
             acc = self.op("mul", a, b) if acc is None else self.op("fma", a, b, acc)
-        for nm, c in sing:
-            if acc is None:
-                acc = nm if c == 1.0 else (self.op("neg", nm) if c == -1.0 else self.op("mul", nm, c))
-                if acc == nm:
-                    acc = ("alias", nm)
-            elif c == 1.0:
-                acc = self.op("add", _reg(acc), nm)
-            elif c == -1.0:
-                acc = self.op("sub", _reg(acc), nm) if not isinstance(acc, float) else self.op("add", self.op("neg", nm), acc)
-            else:
-                acc = self.op("fma", nm, c, _reg(acc))
-        if isinstance(acc, tuple):  # one unscaled single plus nothing else cannot reach here
-            acc = acc[1]
         return Var(acc)
 
     def vec(self, rows, hint=None):
         return [self.lin(r, hint=hint) for r in rows]
-
-
-def _reg(acc):
-    return acc[1] if isinstance(acc, tuple) else acc
 
 
 # ---------------------------------------------------------------------------
