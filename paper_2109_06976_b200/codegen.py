@@ -852,7 +852,8 @@ def split_columns(em, by_task=False):
     each of them; inputs and joint transforms are re-materialised on the
     column side.  nx = number of export slots.
 
-    by_task: `columns` is a list with one program per gradient column task;
+    by_task: `columns` is a list with one program per gradient column task
+    (an int k: k programs, each a run of consecutive column tasks);
     the joints' sin/cos are exported too (each column program would otherwise
     evaluate every joint's sincos), and each program keeps only the input
     loads / transform entries its column uses."""
@@ -902,8 +903,11 @@ def split_columns(em, by_task=False):
                 ctasks.append(em.tasks[i])
         return _sub_emit(em, pops, ptasks), _sub_emit(em, cops, ctasks), len(exports)
     progs = []
-    for task in dict.fromkeys(t for t in em.tasks if t.startswith("grad.")):
-        idx = [i for i, t in enumerate(em.tasks) if t == task]
+    tasks = list(dict.fromkeys(t for t in em.tasks if t.startswith("grad.")))
+    ng = len(tasks) if by_task is True else max(1, min(int(by_task), len(tasks)))
+    groups = [set(tasks[g * len(tasks) // ng:(g + 1) * len(tasks) // ng]) for g in range(ng)]
+    for group in groups:
+        idx = [i for i, t in enumerate(em.tasks) if t in group]
         need = {r for i in idx for r in op_srcs(em.ops[i])}
         keep = set()
         for i in range(len(em.ops) - 1, -1, -1):  # remat ops this column uses, transitively
@@ -1631,7 +1635,7 @@ def _big_part_unit(model, alg, dt, tag, K, tn, trees, zero_fill, fx):
     algorithms run warp-specialised as a whole."""
     if alg in ("gradID", "gradFD") and tn.get("split", True):
         em = generate_knot(model, alg, dt, trees, zero_fill, fext=fx, lowmem=True)
-        by_task = bool(tn.get("split_by_task"))
+        by_task = tn.get("split_by_task") or False
         pre, progs, nx = split_columns(em, by_task=by_task)
         pf = {"park": False, "prefetch_dist": int(tn.get("split_pf_dist", 96)),
               "prefetch_slack": int(tn.get("split_pf_slack", 12)), "ra_budget": int(tn.get("split_budget", 0))}

@@ -1,5 +1,5 @@
-for dt in f64 f32; do VARIANTS=tools/variants_h30.txt bash tools/variants.sh time humanoid30 gradFD $dt 256 1024 2048 4096 8192 2>&1 | python -c "
+VARIANTS=tools/variants_h30.txt bash tools/variants.sh time humanoid30 gradFD f64 262144 2>&1 | python -c "
 import sys, json
 for l in sys.stdin:
-    try: d=json.loads(l); print(d['robot'], d['alg'], d['dtype'], d['N'], d['tuning'], round(d['us'],2))
-    except Exception: print(l[:200])"; done
+    try: d=json.loads(l); print(d['dtype'], d['tuning'], round(d['us'],1), '%.3g'%d['knots_per_s'])
+    except Exception: print(l[:200])"
