@@ -346,7 +346,10 @@ def run_ours(args):
                 "c_abi_ms_per_step": e2e_c * 1e3,
                 # PCIe-bound: host<->device bytes per step over the step time
                 "io_gbs": (h2d + d2h) / e2e_s / 1e9},
-        "roofline": {"bound": "fp64" if dt == "f64" else "fp32", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "fp64" if dt == "f64" else "fp32",
+                     "bound_note": "CUDA-core FMA pipe (no tensor-core work: 6-vector / 6x6 spatial algebra "
+                                   "in fp64); HBM fraction reported alongside as hbm_frac",
+                     "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
                      "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes": alg_bytes,
                      "hbm_gbs": alg_bytes / (ms * 1e-3) / 1e9,
