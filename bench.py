@@ -260,9 +260,15 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # RBD_BENCH_SHARED_GPU=1: every rank on cuda:0 with gloo plumbing -- only
+    # to exercise the multi-rank code path on a one-GPU box (not a scaling run)
+    shared = os.environ.get("RBD_BENCH_SHARED_GPU") == "1"
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(0 if shared else local)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
 
@@ -280,7 +286,7 @@ def run_ours(args):
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -289,7 +295,7 @@ def run_ours(args):
 
     # -- headline, kernel only ---------------------------------------------------
     barrier()
-    with Clocks(local) as clk:
+    with Clocks(0 if shared else local) as clk:
         ms = device_rate(torch, lib, robot, alg, dt, N, args.steps, args.warmup, stream)
     barrier()
     ms = max_over_ranks(ms)
