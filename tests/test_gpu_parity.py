@@ -79,6 +79,30 @@ def test_large_batch_mapping_matches_reference(name, dt):
             assert rel_err(v, refs[nm]) < TOL[dt], (name, alg, dt, nm, rel_err(v, refs[nm]))
 
 
+@pytest.mark.parametrize("name", MODELS)
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_mid_batch_mapping(name, dt):
+    """Mid-size batches (below the large-batch threshold, several CTAs of the
+    warp-specialised kernel, ragged last group): golden knots tiled to
+    N = 1000, gradFD."""
+    g = golden(name)
+    m = models.load(name)
+    N = 1000
+    reps = -(-N // g["q"].shape[0])
+    tile = lambda x: np.tile(x, (reps, 1))[:N]
+    if dt == "f64":
+        q, qd, u = (tile(g[k]) for k in ("q", "qd", "u"))
+        refs = {nm: tile(g[f"gradFD.{nm}"]) for nm, _ in codegen.outputs("gradFD", m.n_dof)}
+    else:
+        q32, qd32, u32 = (g[k].astype(np.float32) for k in ("q", "qd", "u"))
+        r = R.evaluate_batch(m, "gradFD", q32.astype(np.float64), qd32.astype(np.float64), u32.astype(np.float64))
+        q, qd, u = tile(q32), tile(qd32), tile(u32)
+        refs = {nm: tile(v) for nm, v in r.items()}
+    out = _device_eval(m, "gradFD", dt, q, qd, u)
+    for nm, v in out.items():
+        assert rel_err(v, refs[nm]) < TOL[dt], (name, dt, nm)
+
+
 @pytest.mark.parametrize("name", ["quad12", "humanoid30"])
 def test_cross_tree_blocks_exact_zero(name):
     g = golden(name)
