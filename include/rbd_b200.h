@@ -37,7 +37,10 @@
  * Errors: every entry returns 0 on success, a cudaError_t value (> 0) from the
  * CUDA runtime, or a negative RBD_E* code for argument errors.  Device
  * entries launch asynchronously on `stream` and never synchronise or allocate.
- * All entries are reentrant; sessions are not shared between host threads.
+ * All entries are reentrant: any host thread may call any entry on any stream
+ * concurrently (per-stream scratch for the split pipeline, an event chain
+ * for the warp-specialised kernels' shared global arena).  A session is
+ * owned by one host thread at a time.
  */
 #ifndef RBD_B200_H
 #define RBD_B200_H
@@ -147,6 +150,20 @@ int rbd_run_host(rbd_session* s, int alg, int dtype, const void* q, const void* 
 int rbd_run_host_fext(rbd_session* s, int alg, int dtype, const void* q, const void* qd,
                       const void* u, const void* f_ext, void* out0, void* out1, void* out2,
                       int64_t N);
+
+/* Several GPUs (knots are independent): slice k of
+ * ceil(N / count) knots runs through sessions[k] (its own device, pipeline and
+ * host thread), all slices concurrently; results land in place.  Returns the
+ * first failing slice's code. */
+int rbd_run_host_multi(rbd_session* const* sessions, int32_t count, int alg, int dtype,
+                       const void* q, const void* qd, const void* u, void* out0, void* out1,
+                       void* out2, int64_t N);
+int rbd_run_host_multi_fext(rbd_session* const* sessions, int32_t count, int alg, int dtype,
+                            const void* q, const void* qd, const void* u, const void* f_ext,
+                            void* out0, void* out1, void* out2, int64_t N);
+
+/* Device ordinal a session was created on. */
+int rbd_session_device(const rbd_session* s, int32_t* device);
 
 /* Device-resident rollouts (the paper's trajectory-optimisation use case):
  * one semi-implicit Euler step for N knots of this robot, device pointers,

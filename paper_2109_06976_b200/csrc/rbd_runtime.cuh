@@ -23,6 +23,8 @@
 #if defined(__CUDACC__)
 #include <chrono>
 #include <mutex>
+#include <thread>
+#include <vector>
 #endif
 
 #include "rbd_b200.h"
@@ -320,12 +322,28 @@ constexpr size_t rbd_smem_bytes() {
            sizeof(short) * (size_t)rbd_nout<K>() * (rbd_ofull<K>() ? 1 : 2);
 }
 
-// per-device cache of (CTAs per SM x SMs) and of the global arena
+// Per-(kernel, device) launch state: occupancy-derived grid and, for the
+// warp-specialised kernel with a global (L2-resident) arena, the arena and
+// the event of its last launch.  Initialised once under the mutex; launches
+// that share the arena are ordered across streams by an event chain, so the
+// entry stays reentrant (any host thread, any stream).
 struct rbd_dev_cache {
+  std::mutex lock;
+  bool ready = false;
   int grid = 0;
   void* arena = nullptr;
-  size_t arena_bytes = 0;
+  cudaEvent_t last = nullptr;  // recorded after the last launch that used the arena
+  bool used = false;
 };
+
+static inline bool rbd_capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &st) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return st != cudaStreamCaptureStatusNone;
+}
 
 template <class K>
 static int rbd_launch_kernel(const void* q, const void* qd, const void* u, const void* fx, void* o0,
@@ -337,54 +355,70 @@ static int rbd_launch_kernel(const void* q, const void* qd, const void* u, const
       (K::E2 > 0 && !o2))
     return RBD_EINVAL;
   constexpr size_t smem = rbd_smem_bytes<K>();
-  if (smem > 48 * 1024) {
-    // the opt-in is per device; remember which devices have it
-    static unsigned long long done = 0ull;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!(done & (1ull << (dev & 63)))) {
-      cudaError_t e;
+  static rbd_dev_cache cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  rbd_dev_cache& c = cache[dev & 63];
+  std::unique_lock<std::mutex> guard(c.lock);
+  if (!c.ready) {
+    cudaError_t e = cudaSuccess;
+    // the large-shared-memory opt-in is per device
+    if (smem > 48 * 1024) {
       if constexpr (K::MAP == 1)
         e = cudaFuncSetAttribute(rbd_ws_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       else
-        e = cudaFuncSetAttribute(rbd_batch_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
+        e = cudaFuncSetAttribute(rbd_batch_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return (int)e;
-      done |= 1ull << (dev & 63);
     }
-  }
-  if constexpr (K::MAP == 1) {
-    static rbd_dev_cache cache[64];
-    int dev = 0;
-    cudaGetDevice(&dev);
-    rbd_dev_cache& c = cache[dev & 63];
-    if (c.grid == 0) {
+    if constexpr (K::MAP == 1) {
       int per_sm = 0, sms = 0;
-      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rbd_ws_kernel<K>, K::W * 32, smem);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rbd_ws_kernel<K>, K::W * 32, smem);
       if (e != cudaSuccess) return (int)e;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      c.grid = (per_sm > 0 ? per_sm : 1) * sms;
+      const int grid = (per_sm > 0 ? per_sm : 1) * sms;
       if (!K::ARENA_SMEM && !K::ARENA_GROUP) {
-        c.arena_bytes = sizeof(T) * (size_t)c.grid * K::NA * 32;
-        e = cudaMalloc(&c.arena, c.arena_bytes);
-        if (e != cudaSuccess) { c.grid = 0; return (int)e; }
+        e = cudaMalloc(&c.arena, sizeof(T) * (size_t)grid * K::NA * 32);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.last, cudaEventDisableTiming);
+        if (e != cudaSuccess) return (int)e;
       }
+      c.grid = grid;
     }
+    c.ready = true;
+  }
+  if constexpr (K::MAP == 1) {
     const long long groups = (N + 31) / 32;
     const long long grid = groups < c.grid ? groups : c.grid;
     if (K::ARENA_GROUP && !xs) return RBD_EINVAL;
-    rbd_ws_kernel<K><<<(unsigned)grid, K::W * 32, smem, (cudaStream_t)stream>>>(
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool shared_arena = !K::ARENA_SMEM && !K::ARENA_GROUP;
+    // the global arena is indexed by CTA: a launch waits for the previous
+    // launch of this kernel (any stream) before reusing it.  Inside a stream
+    // capture the graph's own order applies (no foreign events in a graph).
+    const bool chain = shared_arena && !rbd_capturing(st);
+    if (!shared_arena) guard.unlock();
+    if (chain && c.used) {
+      cudaError_t e = cudaStreamWaitEvent(st, c.last, 0);
+      if (e != cudaSuccess) return (int)e;
+    }
+    rbd_ws_kernel<K><<<(unsigned)grid, K::W * 32, smem, st>>>(
         (const T*)q, (const T*)qd, (const T*)u, (const T*)fx, (T*)o0, (T*)o1, (T*)o2, (long long)N,
         K::ARENA_GROUP ? (T*)xs : (T*)c.arena);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess && chain) {
+      e = cudaEventRecord(c.last, st);
+      c.used = true;
+    }
+    return (int)e;
   } else {
+    guard.unlock();
     const long long grid = (N + K::BK - 1) / K::BK;
     if (K::NX && !xs) return RBD_EINVAL;
     // several programs (split gradient columns): grid row y runs program y
     rbd_batch_kernel<K><<<dim3((unsigned)grid, rbd_nprog<K>()), K::BK, smem, (cudaStream_t)stream>>>(
         (const T*)q, (const T*)qd, (const T*)u, (const T*)fx, (T*)o0, (T*)o1, (T*)o2, (long long)N,
         (T*)xs);
+    return (int)cudaGetLastError();
   }
-  return (int)cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -394,35 +428,69 @@ static int rbd_launch_kernel(const void* q, const void* qd, const void* u, const
 // knot) reloads them through its register plan.  Chunks of KA::CHUNK knots
 // keep the scratch L2-resident.
 // ---------------------------------------------------------------------------
-// Per-device side streams and events of the split pipeline (created once).
+// Side streams, events and the double-buffered scratch of the split
+// pipeline, one set per (device, caller stream): calls from different
+// streams (or host threads) never share a scratch buffer, and calls on one
+// caller stream are ordered by that stream (each call forks from it and
+// joins back into it), so the pipeline is reentrant.
 struct rbd_split_state {
   bool init = false;
+  int dev = -1;
+  cudaStream_t caller = nullptr;
   void* scratch[2] = {nullptr, nullptr};
   size_t bytes = 0;
   cudaStream_t sa = nullptr, sb = nullptr;
-  cudaEvent_t start = nullptr, done_a[2] = {nullptr, nullptr}, done_b[2] = {nullptr, nullptr};
+  cudaEvent_t start = nullptr, join_a = nullptr, join_b = nullptr;
+  cudaEvent_t done_a[2] = {nullptr, nullptr}, done_b[2] = {nullptr, nullptr};
+  bool recorded[2] = {false, false};  // done_b[b] marks the last read of scratch[b]
+  std::mutex lock;
 };
+#define RBD_SPLIT_STATES 64
 
 template <class KA, class KB>
-static rbd_split_state& rbd_split_state_of(int dev) {
-  static rbd_split_state state[64];
-  return state[dev & 63];
+static rbd_split_state* rbd_split_state_of(int dev, cudaStream_t caller, bool create) {
+  static rbd_split_state state[RBD_SPLIT_STATES];
+  static std::mutex table;
+  std::lock_guard<std::mutex> g(table);
+  for (auto& st : state)
+    if (st.init && st.dev == dev && st.caller == caller) return &st;
+  if (!create) return nullptr;
+  for (auto& st : state) {
+    if (st.init) continue;
+    constexpr size_t bytes = sizeof(typename KA::T) * (size_t)KA::CHUNK * KA::NX;
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaMalloc(&st.scratch[i], bytes);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st.sa, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st.sb, cudaStreamNonBlocking);
+    cudaEvent_t* evs[] = {&st.start, &st.join_a, &st.join_b, &st.done_a[0], &st.done_a[1], &st.done_b[0],
+                          &st.done_b[1]};
+    for (cudaEvent_t* ev : evs)
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return nullptr;
+    st.bytes = bytes;
+    st.dev = dev;
+    st.caller = caller;
+    st.init = true;
+    return &st;
+  }
+  return nullptr;  // more than RBD_SPLIT_STATES distinct caller streams
 }
 
-// Join: the caller's stream continues after both side streams of the split
+// Join: the caller's stream continues after both side streams of its split
 // pipeline on the current device.
 template <class KA, class KB>
 static int rbd_split_join(void* stream) {
   int dev = 0;
   cudaGetDevice(&dev);
-  rbd_split_state& st = rbd_split_state_of<KA, KB>(dev);
-  if (!st.init) return 0;
+  rbd_split_state* st = rbd_split_state_of<KA, KB>(dev, (cudaStream_t)stream, false);
+  if (!st) return 0;
+  std::lock_guard<std::mutex> guard(st->lock);
   cudaStream_t s0 = (cudaStream_t)stream;
   cudaError_t e;
-  if ((e = cudaEventRecord(st.done_a[0], st.sa)) != cudaSuccess) return (int)e;
-  if ((e = cudaStreamWaitEvent(s0, st.done_a[0], 0)) != cudaSuccess) return (int)e;
-  if ((e = cudaEventRecord(st.done_b[0], st.sb)) != cudaSuccess) return (int)e;
-  if ((e = cudaStreamWaitEvent(s0, st.done_b[0], 0)) != cudaSuccess) return (int)e;
+  if ((e = cudaEventRecord(st->join_a, st->sa)) != cudaSuccess) return (int)e;
+  if ((e = cudaStreamWaitEvent(s0, st->join_a, 0)) != cudaSuccess) return (int)e;
+  if ((e = cudaEventRecord(st->join_b, st->sb)) != cudaSuccess) return (int)e;
+  if ((e = cudaStreamWaitEvent(s0, st->join_b, 0)) != cudaSuccess) return (int)e;
   return 0;
 }
 
@@ -438,54 +506,47 @@ static int rbd_launch_split(const void* q, const void* qd, const void* u, const 
   static_assert(KA::CHUNK % KA::BK == 0 && KA::BK % 32 == 0, "chunk / CTA / warp alignment");
   if (N < 0) return RBD_EINVAL;
   if (N == 0) return 0;
-  static std::mutex lock;  // host side: the shared events / side streams of one device
-  std::lock_guard<std::mutex> guard(lock);
   int dev = 0;
   cudaGetDevice(&dev);
-  rbd_split_state& st = rbd_split_state_of<KA, KB>(dev);
-  const size_t bytes = sizeof(T) * (size_t)KA::CHUNK * KA::NX;
-  if (!st.init) {
-    cudaError_t e = cudaSuccess;
-    for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaMalloc(&st.scratch[i], bytes);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st.sa, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st.sb, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&st.start, cudaEventDisableTiming);
-    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
-      e = cudaEventCreateWithFlags(&st.done_a[i], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&st.done_b[i], cudaEventDisableTiming);
-    }
-    if (e != cudaSuccess) return (int)e;
-    st.bytes = bytes;
-    st.init = true;
-  }
-  if (st.bytes < bytes) return RBD_EINVAL;  // one split kernel pair per (device, scratch size) class
-  // pipeline over two scratch buffers: prefix(i+1) on stream A overlaps
-  // columns(i) on stream B; A reuses buffer b only after B has read it
   cudaStream_t s0 = (cudaStream_t)stream;
-  cudaError_t e = cudaEventRecord(st.start, s0);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(st.sa, st.start, 0);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(st.sb, st.start, 0);
-  if (e != cudaSuccess) return (int)e;
-  constexpr int n = KA::NDOF;
-  int chunk = 0;
-  for (int64_t c0 = 0; c0 < N; c0 += KA::CHUNK, ++chunk) {
-    const int buf = chunk & 1;
-    const int64_t nk = (N - c0) < KA::CHUNK ? (N - c0) : KA::CHUNK;
-    const T* cq = (const T*)q + c0 * n;
-    const T* cqd = qd ? (const T*)qd + c0 * n : nullptr;
-    const T* cu = u ? (const T*)u + c0 * n : nullptr;
-    const T* cfx = fx ? (const T*)fx + c0 * 6 * n : nullptr;
-    T* c_o0 = (T*)o0 + c0 * KA::E0;
-    T* c_o1 = KA::E1 ? (T*)o1 + c0 * KA::E1 : nullptr;
-    T* c_o2 = KA::E2 ? (T*)o2 + c0 * KA::E2 : nullptr;
-    if (chunk >= 2 && (e = cudaStreamWaitEvent(st.sa, st.done_b[buf], 0)) != cudaSuccess) return (int)e;
-    int rc = rbd_launch_kernel<KA>(cq, cqd, cu, cfx, c_o0, c_o1, c_o2, nk, (void*)st.sa, st.scratch[buf]);
-    if (rc) return rc;
-    if ((e = cudaEventRecord(st.done_a[buf], st.sa)) != cudaSuccess) return (int)e;
-    if ((e = cudaStreamWaitEvent(st.sb, st.done_a[buf], 0)) != cudaSuccess) return (int)e;
-    rc = rbd_launch_kernel<KB>(cq, cqd, cu, cfx, c_o0, c_o1, c_o2, nk, (void*)st.sb, st.scratch[buf]);
-    if (rc) return rc;
-    if ((e = cudaEventRecord(st.done_b[buf], st.sb)) != cudaSuccess) return (int)e;
+  rbd_split_state* stp = rbd_split_state_of<KA, KB>(dev, s0, true);
+  if (!stp) return (int)cudaErrorMemoryAllocation;
+  rbd_split_state& st = *stp;
+  {
+    std::lock_guard<std::mutex> guard(st.lock);
+    // pipeline over two scratch buffers: prefix(i+1) on stream A overlaps
+    // columns(i) on stream B; A reuses buffer b only after B has read it
+    cudaError_t e = cudaEventRecord(st.start, s0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st.sa, st.start, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st.sb, st.start, 0);
+    if (e != cudaSuccess) return (int)e;
+    constexpr int n = KA::NDOF;
+    // two host threads on one caller stream: the previous call's column
+    // kernels may still read the scratch (outside a capture only; a graph
+    // orders its own nodes)
+    const bool ext = !rbd_capturing(s0);
+    int chunk = 0;
+    for (int64_t c0 = 0; c0 < N; c0 += KA::CHUNK, ++chunk) {
+      const int buf = chunk & 1;
+      const int64_t nk = (N - c0) < KA::CHUNK ? (N - c0) : KA::CHUNK;
+      const T* cq = (const T*)q + c0 * n;
+      const T* cqd = qd ? (const T*)qd + c0 * n : nullptr;
+      const T* cu = u ? (const T*)u + c0 * n : nullptr;
+      const T* cfx = fx ? (const T*)fx + c0 * 6 * n : nullptr;
+      T* c_o0 = (T*)o0 + c0 * KA::E0;
+      T* c_o1 = KA::E1 ? (T*)o1 + c0 * KA::E1 : nullptr;
+      T* c_o2 = KA::E2 ? (T*)o2 + c0 * KA::E2 : nullptr;
+      if ((chunk >= 2 || (ext && st.recorded[buf])) && (e = cudaStreamWaitEvent(st.sa, st.done_b[buf], 0)) != cudaSuccess)
+        return (int)e;
+      int rc = rbd_launch_kernel<KA>(cq, cqd, cu, cfx, c_o0, c_o1, c_o2, nk, (void*)st.sa, st.scratch[buf]);
+      if (rc) return rc;
+      if ((e = cudaEventRecord(st.done_a[buf], st.sa)) != cudaSuccess) return (int)e;
+      if ((e = cudaStreamWaitEvent(st.sb, st.done_a[buf], 0)) != cudaSuccess) return (int)e;
+      rc = rbd_launch_kernel<KB>(cq, cqd, cu, cfx, c_o0, c_o1, c_o2, nk, (void*)st.sb, st.scratch[buf]);
+      if (rc) return rc;
+      if ((e = cudaEventRecord(st.done_b[buf], st.sb)) != cudaSuccess) return (int)e;
+      st.recorded[buf] = ext;
+    }
   }
   return join ? rbd_split_join<KA, KB>(stream) : 0;
 }
@@ -735,6 +796,77 @@ extern "C" int rbd_run_host_fext(rbd_session* s, int alg, int dtype, const void*
                                  void* out2, int64_t N) {
   if (!f_ext) return RBD_EINVAL;
   return rbd_run_host_impl(s, alg, dtype, q, qd, u, f_ext, out0, out1, out2, N);
+}
+
+// ---------------------------------------------------------------------------
+// several devices: one session per device, contiguous batch slices
+// ---------------------------------------------------------------------------
+// Knots are independent (no exchange step): slice k of ceil(N / count) knots
+// runs on session k's device from its own host thread, through that
+// session's own pipeline; results land in place in the caller's arrays.
+static void rbd_shard(int64_t N, int32_t count, int32_t k, int64_t* begin, int64_t* len) {
+  const int64_t per = (N + count - 1) / count;
+  int64_t b = per * k;
+  if (b > N) b = N;
+  int64_t e = b + per;
+  if (e > N) e = N;
+  *begin = b;
+  *len = e - b;
+}
+
+static int rbd_run_host_multi_impl(rbd_session* const* s, int32_t count, int alg, int dtype, const void* q,
+                                   const void* qd, const void* u, const void* fx, void* out0, void* out1,
+                                   void* out2, int64_t N) {
+  if (!s || count <= 0) return RBD_EINVAL;
+  for (int32_t k = 0; k < count; ++k)
+    if (!s[k]) return RBD_ESESSION;
+  const rbd_entry* e = rbd_entry_for(alg, dtype, fx ? 1 : 0);
+  if (!e || N < 0) return RBD_EINVAL;
+  const int64_t n = rbd_ndof();
+  const size_t es = (size_t)e->elem;
+  const int64_t iext[4] = {n, n, n, 6 * n};
+  const int64_t ext[3] = {e->e0, e->e1, e->e2};
+  std::vector<int> rc(count, 0);
+  std::vector<std::thread> th;
+  for (int32_t k = 0; k < count; ++k) {
+    int64_t b, len;
+    rbd_shard(N, count, k, &b, &len);
+    if (len == 0) continue;
+    auto in = [&](const void* p, int a) -> const void* {
+      return p ? (const unsigned char*)p + (size_t)(b * iext[a]) * es : nullptr;
+    };
+    auto out = [&](void* p, int j) -> void* {
+      return (p && ext[j]) ? (unsigned char*)p + (size_t)(b * ext[j]) * es : nullptr;
+    };
+    const void *kq = in(q, 0), *kqd = in(qd, 1), *ku = in(u, 2), *kfx = in(fx, 3);
+    void *k0 = out(out0, 0), *k1 = out(out1, 1), *k2 = out(out2, 2);
+    th.emplace_back([=, &rc]() {
+      rc[k] = rbd_run_host_impl(s[k], alg, dtype, kq, kqd, ku, kfx, k0, k1, k2, len);
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int32_t k = 0; k < count; ++k)
+    if (rc[k]) return rc[k];
+  return 0;
+}
+
+extern "C" int rbd_run_host_multi(rbd_session* const* sessions, int32_t count, int alg, int dtype,
+                                  const void* q, const void* qd, const void* u, void* out0, void* out1,
+                                  void* out2, int64_t N) {
+  return rbd_run_host_multi_impl(sessions, count, alg, dtype, q, qd, u, nullptr, out0, out1, out2, N);
+}
+
+extern "C" int rbd_run_host_multi_fext(rbd_session* const* sessions, int32_t count, int alg, int dtype,
+                                       const void* q, const void* qd, const void* u, const void* f_ext,
+                                       void* out0, void* out1, void* out2, int64_t N) {
+  if (!f_ext) return RBD_EINVAL;
+  return rbd_run_host_multi_impl(sessions, count, alg, dtype, q, qd, u, f_ext, out0, out1, out2, N);
+}
+
+extern "C" int rbd_session_device(const rbd_session* s, int32_t* device) {
+  if (!s || !device) return RBD_ESESSION;
+  *device = s->device;
+  return 0;
 }
 
 // ---------------------------------------------------------------------------

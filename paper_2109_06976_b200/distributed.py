@@ -56,8 +56,24 @@ def run_sharded(evaluate, arrays, group=None, gather_result=False):
     return outs, bounds
 
 
+def evaluate_sharded(fn, model, *arrays, group=None, gather_result=False, **kw):
+    """This rank's contiguous slice of a batch through a drop-in dynamics
+    entry (`fn` = dynamics.fd_grad, rnea, ...) on this rank's device -- the
+    generated kernels, one process per GPU, no collective on the hot path;
+    with gather_result, the outputs are all-gathered to the full batch (NCCL
+    over NVLink for CUDA tensors, gloo for host tensors)."""
+    def evaluate(parts):
+        out = fn(model, *parts, **kw)
+        if hasattr(out, "dq"):
+            out = [out.dq, out.dqd] + ([out.qdd] if out.qdd is not None else [])
+        elif not isinstance(out, (list, tuple)):
+            out = [out]
+        return list(out)
+    return run_sharded(evaluate, list(arrays), group=group, gather_result=gather_result)
+
+
 def split_even(N, parts):
     return [shard_bounds(N, parts, r) for r in range(parts)]
 
 
-__all__ = ["shard_bounds", "shard", "gather", "run_sharded", "split_even", "np"]
+__all__ = ["shard_bounds", "shard", "gather", "run_sharded", "evaluate_sharded", "split_even", "np"]

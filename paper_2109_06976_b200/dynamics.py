@@ -26,6 +26,9 @@ inputs containing non-finite values raise ValueError too.  `f_ext` (per-link
 external forces in link coordinates, refdyn.py:79-80) is `(n, 6)` for one
 knot or `(N, n, 6)`, and runs the f_ext kernels (`rbd_<alg>_<dt>_fext`; the
 reference's generated programs have no f_ext input, its refdyn does).
+`devices=[0, 1, ...]` slices a host batch across several GPUs (contiguous
+ceil(N / G) slices, one session and host thread per GPU, results in place;
+knots are independent, so there is no exchange step).
 """
 
 from dataclasses import dataclass
@@ -89,9 +92,30 @@ def _fext_shape(model, fx, single, N):
         raise ValueError(f"f_ext has shape {shp}, expected {want}")
 
 
-def _run(model, alg, args, dtype=None, device=None, f_ext=None):
+_PIN_BYTES = 1 << 20  # host outputs at least this large come from the pinned pool
+
+
+def _host_empty(shape, ndt):
+    """Output array for the host path.  Large outputs are page-locked, taken
+    from torch's caching pinned-host allocator (blocks return to the pool
+    when the array is freed), so the D2H copies run at full PCIe speed
+    instead of through pageable staging."""
+    nbytes = int(np.prod(shape)) * np.dtype(ndt).itemsize
+    if nbytes >= _PIN_BYTES:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                tdt = torch.float32 if ndt == np.float32 else torch.float64
+                return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
+        except Exception:
+            pass
+    return np.empty(shape, dtype=ndt)
+
+
+def _run(model, alg, args, dtype=None, device=None, f_ext=None, devices=None):
     """Evaluate `alg` on state arguments `args` (1 or 3 arrays), optionally
-    with per-link external forces f_ext."""
+    with per-link external forces f_ext; host arrays may be sliced across
+    several GPUs (`devices`)."""
     dt = _resolve_dtype(args, dtype)
     on_device = _is_torch(args[0]) and args[0].is_cuda
     lib = runtime.robot_library(model)
@@ -112,6 +136,8 @@ def _run(model, alg, args, dtype=None, device=None, f_ext=None):
                 raise ValueError("mixing device and host state arguments")
             fx = f_ext.to(tdt).contiguous()
             _fext_shape(model, fx, single, N)
+        if devices:
+            raise ValueError("devices= applies to host arrays; a CUDA tensor runs on its own device")
         outs = [torch.empty((N, e), dtype=tdt, device=dev) for _, e in codegen.outputs(alg, n)]
         with torch.cuda.device(dev):
             stream = torch.cuda.current_stream(dev).cuda_stream
@@ -137,8 +163,8 @@ def _run(model, alg, args, dtype=None, device=None, f_ext=None):
         for x in xs_check:
             if not np.all(np.isfinite(x)):
                 raise ValueError("state vector contains non-finite entries")
-        outs = [np.empty((N, e), dtype=ndt) for _, e in codegen.outputs(alg, n)]
-        runtime.run_host(lib, alg, dt, xs, outs, N, device=device, f_ext=fx)
+        outs = [_host_empty((N, e), ndt) for _, e in codegen.outputs(alg, n)]
+        runtime.run_host(lib, alg, dt, xs, outs, N, device=device, f_ext=fx, devices=devices)
     shaped = []
     for (nm, e), o in zip(codegen.outputs(alg, n), outs):
         shp = (n, n) if e == n * n else (n,)
@@ -146,39 +172,39 @@ def _run(model, alg, args, dtype=None, device=None, f_ext=None):
     return shaped
 
 
-def rnea(model, q, qd, qdd, f_ext=None, dtype=None):
+def rnea(model, q, qd, qdd, f_ext=None, dtype=None, devices=None):
     """Inverse dynamics (reference `refdyn.py:91-94`)."""
-    return _run(model, "ID", [q, qd, qdd], dtype, f_ext=f_ext)[0]
+    return _run(model, "ID", [q, qd, qdd], dtype, f_ext=f_ext, devices=devices)[0]
 
 
-def bias_force(model, q, qd, f_ext=None, dtype=None):
+def bias_force(model, q, qd, f_ext=None, dtype=None, devices=None):
     """rnea at qdd = 0 (reference `refdyn.py:97-100`)."""
     if _is_torch(q):
         import torch
         zero = torch.zeros_like(q)
     else:
         zero = np.zeros_like(np.asarray(q, dtype=np.float32 if _resolve_dtype([q], dtype) == "f32" else np.float64))
-    return _run(model, "ID", [q, qd, zero], dtype, f_ext=f_ext)[0]
+    return _run(model, "ID", [q, qd, zero], dtype, f_ext=f_ext, devices=devices)[0]
 
 
-def minv_direct(model, q, dtype=None):
+def minv_direct(model, q, dtype=None, devices=None):
     """Direct inverse mass matrix (reference `refdyn.py:128-169`)."""
-    return _run(model, "Minv", [q], dtype)[0]
+    return _run(model, "Minv", [q], dtype, devices=devices)[0]
 
 
-def forward_dynamics(model, q, qd, tau, f_ext=None, dtype=None):
+def forward_dynamics(model, q, qd, tau, f_ext=None, dtype=None, devices=None):
     """qdd = Minv (tau - c) (reference `refdyn.py:172-175`)."""
-    return _run(model, "FD", [q, qd, tau], dtype, f_ext=f_ext)[0]
+    return _run(model, "FD", [q, qd, tau], dtype, f_ext=f_ext, devices=devices)[0]
 
 
-def rnea_grad(model, q, qd, qdd, f_ext=None, dtype=None):
+def rnea_grad(model, q, qd, qdd, f_ext=None, dtype=None, devices=None):
     """(dtau/dq, dtau/dqd) (reference `refdyn.py:178-239`)."""
-    dq, dqd = _run(model, "gradID", [q, qd, qdd], dtype, f_ext=f_ext)
+    dq, dqd = _run(model, "gradID", [q, qd, qdd], dtype, f_ext=f_ext, devices=devices)
     return DynamicsGradients(dq, dqd)
 
 
-def fd_grad(model, q, qd, tau, f_ext=None, dtype=None):
+def fd_grad(model, q, qd, tau, f_ext=None, dtype=None, devices=None):
     """(dqdd/dq, dqdd/dqd) = -Minv dID at qdd = FD(q, qd, tau)
     (reference `refdyn.py:242-249`); the solved qdd rides along."""
-    dq, dqd, qdd = _run(model, "gradFD", [q, qd, tau], dtype, f_ext=f_ext)
+    dq, dqd, qdd = _run(model, "gradFD", [q, qd, tau], dtype, f_ext=f_ext, devices=devices)
     return DynamicsGradients(dq, dqd, qdd)

@@ -95,7 +95,31 @@ def load_text(text):
             phases[-1][1].append(item)
         else:
             raise KernelFormatError(f"bad dump line: {ln!r}")
-    return Program(arena, inputs, outputs, phases, meta)
+    prog = Program(arena, inputs, outputs, phases, meta)
+    validate_program(prog)
+    return prog
+
+
+def validate_program(prog):
+    """Structural checks of a parsed dump, restating the reference's
+    `validate_program` (ir.py:79-99): a non-empty phase list, every input /
+    output segment inside the arena, every instruction slot (destination and
+    sources; a load_const's immediate excepted) in [0, arena_size).  A
+    truncated or corrupted dump raises here instead of compiling into a
+    kernel that silently reads zeros."""
+    if not prog.phases:
+        raise KernelFormatError("program has no phases")
+    size = prog.arena_size
+    for name, (off, ext) in list(prog.input_map.items()) + list(prog.output_map.items()):
+        if not (0 <= off and off + ext <= size):
+            raise KernelFormatError(f"segment {name!r} outside arena")
+    for pi, (_, items) in enumerate(prog.phases):
+        for wi, item in enumerate(items):
+            for ins in item:
+                slots = ins[1:2] if ins[0] == "load_const" else ins[1:]
+                for sl in slots:
+                    if not (0 <= sl < size):
+                        raise KernelFormatError(f"phase {pi} item {wi}: slot {sl} outside arena of {size}")
 
 
 def to_emit(prog, dtype="f64"):

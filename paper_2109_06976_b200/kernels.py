@@ -143,6 +143,7 @@ class RbdInfo(ctypes.Structure):
 
 ABI_SYMBOLS = (["rbd_get_info", "rbd_alg_extents", "rbd_launch", "rbd_launch_fext", "rbd_session_create",
                 "rbd_session_destroy", "rbd_run_host", "rbd_run_host_fext", "rbd_bench_host",
+                "rbd_run_host_multi", "rbd_run_host_multi_fext", "rbd_session_device",
                 "rbd_euler_step"]
                + [f"rbd_{a}_{d}" for a in codegen.ALGORITHMS for d in codegen.DTYPES]
                + [f"rbd_{a}_{d}_fext" for a in codegen.FEXT_ALGORITHMS for d in codegen.DTYPES])
@@ -159,6 +160,11 @@ def _bind(lib):
     lib.rbd_run_host_fext.argtypes = [_vp, ctypes.c_int, ctypes.c_int] + [_vp] * 7 + [ctypes.c_int64]
     lib.rbd_session_create.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(_vp)]
     lib.rbd_session_destroy.argtypes = [_vp]
+    lib.rbd_session_device.argtypes = [_vp, ctypes.POINTER(ctypes.c_int32)]
+    lib.rbd_run_host_multi.argtypes = [ctypes.POINTER(_vp), ctypes.c_int32, ctypes.c_int, ctypes.c_int] + [_vp] * 6 \
+        + [ctypes.c_int64]
+    lib.rbd_run_host_multi_fext.argtypes = [ctypes.POINTER(_vp), ctypes.c_int32, ctypes.c_int, ctypes.c_int] \
+        + [_vp] * 7 + [ctypes.c_int64]
     lib.rbd_run_host.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64]
     lib.rbd_bench_host.argtypes = ([_vp, ctypes.c_int, ctypes.c_int] + [_vp] * 6
                                    + [ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)])

@@ -111,24 +111,70 @@ _SESSIONS = {}
 def default_chunk(lib):
     """~64 MiB of fp64 per pipeline stage."""
     worst = 0
+    info = kernels.RbdInfo()
+    lib.rbd_get_info(ctypes.byref(info))
     for a in range(5):
         ni, e0, e1, e2 = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         lib.rbd_alg_extents(a, ctypes.byref(ni), ctypes.byref(e0), ctypes.byref(e1), ctypes.byref(e2))
-        info = kernels.RbdInfo()
-        lib.rbd_get_info(ctypes.byref(info))
         worst = max(worst, ni.value * info.n_dof + e0.value + e1.value + e2.value)
     return max(4096, min(1 << 20, (64 << 20) // (8 * max(worst, 1))))
 
 
-def session(lib, device=0):
-    key = (id(lib), device)
+def current_device():
+    """The caller's current CUDA device (torch's, when torch is in use), else 0."""
+    import sys
+    torch = sys.modules.get("torch")
+    if torch is not None:
+        try:
+            if torch.cuda.is_initialized():
+                return torch.cuda.current_device()
+        except Exception:
+            pass
+    return 0
+
+
+def session(lib, device=None, lane=0):
+    """The calling host thread's session on `device` (default: the current
+    device).  Sessions own pinned staging and device buffers, so each host
+    thread gets its own (the C ABI's rule: a session is not shared between
+    threads); `lane` tells apart the sessions of one multi-device call (a
+    device may appear twice in its list).  They live as long as the library."""
+    dev = current_device() if device is None else int(device)
+    key = (id(lib), dev, threading.get_ident(), lane)
     with _SESS_LOCK:
         s = _SESSIONS.get(key)
         if s is None:
-            s = Session(lib, device, default_chunk(lib))
+            s = Session(lib, dev, default_chunk(lib))
             _SESSIONS[key] = s
         return s
 
 
-def run_host(lib, alg, dtype, in_arrays, out_arrays, N, device=None, f_ext=None):
-    session(lib, 0 if device is None else device).run(alg, dtype, in_arrays, out_arrays, N, f_ext)
+def shard_ranges(N, count):
+    """Contiguous slices [(begin, length)] of ceil(N / count) knots -- the
+    split rbd_run_host_multi makes (rbd_runtime.cuh rbd_shard)."""
+    per = -(-int(N) // int(count)) if count > 0 else 0
+    out = []
+    for k in range(count):
+        b = min(per * k, N)
+        out.append((b, min(b + per, N) - b))
+    return out
+
+
+def run_host(lib, alg, dtype, in_arrays, out_arrays, N, device=None, f_ext=None, devices=None):
+    """Host buffers through the library's pipeline.  devices=[d0, d1, ...]:
+    the batch is sliced across those GPUs (rbd_run_host_multi: one session
+    and host thread per device, slices run concurrently)."""
+    if not devices or len(devices) == 1:
+        dev = devices[0] if devices else device
+        session(lib, dev).run(alg, dtype, in_arrays, out_arrays, N, f_ext)
+        return
+    sess = [session(lib, d, lane=1 + k) for k, d in enumerate(devices)]
+    arr = (ctypes.c_void_p * len(sess))(*[s.handle.value for s in sess])
+    ins = [a.ctypes.data_as(ctypes.c_void_p) for a in in_arrays] + [None] * (3 - len(in_arrays))
+    outs = [a.ctypes.data_as(ctypes.c_void_p) for a in out_arrays] + [None] * (3 - len(out_arrays))
+    if f_ext is not None:
+        rc = lib.rbd_run_host_multi_fext(arr, len(sess), _ALG_ID[alg], _DT_ID[dtype], *ins,
+                                         f_ext.ctypes.data_as(ctypes.c_void_p), *outs, ctypes.c_int64(N))
+    else:
+        rc = lib.rbd_run_host_multi(arr, len(sess), _ALG_ID[alg], _DT_ID[dtype], *ins, *outs, ctypes.c_int64(N))
+    check(rc, f"rbd_run_host_multi({alg}, {dtype}, {len(sess)} devices)")

@@ -223,15 +223,26 @@ def test_fext_matches_reference(name, dt):
         assert rel_err(one[None], g["fext.ID.tau_out"][:1]) < 1e-9
 
 
-@pytest.mark.parametrize("name,dt", [("chain7", "f64"), ("chain7", "f32"), ("humanoid30", "f64")])
-def test_full_size_properties(name, dt):
-    """BASELINE full size (N = 2^20): sampled knots vs the oracle plus
+FULL_SIZE = [("chain7", "f64", 1 << 20), ("chain7", "f32", 1 << 20),
+             ("quad12", "f64", 1 << 20), ("quad12", "f32", 1 << 20),
+             ("humanoid30", "f64", 1 << 18), ("humanoid30", "f32", 1 << 18),
+             ("humanoid30", "f64", 1 << 20), ("humanoid30", "f32", 1 << 20)]
+
+
+@pytest.mark.parametrize("name,dt,N", FULL_SIZE)
+def test_full_size_properties(name, dt, N):
+    """Every benchmarked large-batch config (BASELINE configs[4] sizes): 64
+    sampled knots of gradFD vs the oracle at the north-star tolerance, plus
     size-independent identities over the whole batch on the device:
-    ID(q, qd, FD(q, qd, tau)) = tau, FD qdd = gradFD qdd, Minv symmetric."""
-    from paper_2109_06976_b200 import runtime
+    ID(q, qd, FD(q, qd, tau)) = tau, FD qdd = gradFD qdd, Minv symmetric,
+    cross-tree blocks of dFD exactly 0.
+
+    The identity tolerance is 1e-9 (fp64) / 1e-4 (fp32) relative to the
+    magnitude of the terms the RNEA sums, max|tau| + max|c(q, qd)|: tau is
+    U(-1, 1) while the bias c reaches tens of N m, so a backward-stable fp32
+    round trip is accurate to eps * |c|, not to eps * |tau|."""
     m = models.load(name)
     n = m.n_dof
-    N = 1 << 20 if name == "chain7" else 1 << 18
     tdt = torch.float64 if dt == "f64" else torch.float32
     gen = torch.Generator(device="cuda").manual_seed(5)
     q = (torch.rand((N, n), generator=gen, device="cuda", dtype=torch.float64) * 2 - 1) * np.pi
@@ -239,20 +250,32 @@ def test_full_size_properties(name, dt):
     tau = torch.rand((N, n), generator=gen, device="cuda", dtype=torch.float64) * 2 - 1
     q, qd, tau = q.to(tdt), qd.to(tdt), tau.to(tdt)
     g = dynamics.fd_grad(m, q, qd, tau)
-    qdd = dynamics.forward_dynamics(m, q, qd, tau)
-    tau2 = dynamics.rnea(m, q, qd, qdd)
-    Mi = dynamics.minv_direct(m, q)
     torch.cuda.synchronize()
-    tol = 1e-9 if dt == "f64" else 2e-3
-    scale = tau.abs().amax(dim=1).clamp_min(1e-30)
-    assert float(((tau2 - tau).abs().amax(dim=1) / scale).max()) < tol
-    assert float(((g.qdd - qdd).abs().amax(dim=1) / qdd.abs().amax(dim=1).clamp_min(1e-30)).max()) < tol
-    assert float((Mi - Mi.transpose(1, 2)).abs().max()) <= (1e-12 if dt == "f64" else 1e-5) * float(Mi.abs().max())
-    idx = torch.randint(0, N, (24,), generator=gen, device="cuda").cpu().numpy()
+    idx = torch.randint(0, N, (64,), generator=gen, device="cuda").cpu().numpy()
+    idx[0], idx[-1] = 0, N - 1  # first and last CTA / chunk
     qs, qds, taus = (x[idx].double().cpu().numpy() for x in (q, qd, tau))
     ref = R.evaluate_batch(m, "gradFD", qs, qds, taus)
     for nm, v in (("dq_out", g.dq), ("dqd_out", g.dqd), ("qdd_out", g.qdd)):
-        assert rel_err(v[idx].reshape(len(idx), -1).double().cpu().numpy(), ref[nm]) < TOL[dt]
+        assert rel_err(v[idx].reshape(len(idx), -1).double().cpu().numpy(), ref[nm]) < TOL[dt], (name, dt, N, nm)
+    blocks = np.zeros((n, n), dtype=bool)
+    for t in m.roots():
+        sub = m.subtree(t)
+        blocks[np.ix_(sub, sub)] = True
+    if not blocks.all():
+        off = torch.from_numpy(~blocks).cuda()
+        assert float(g.dq[:, off].abs().max()) == 0.0 and float(g.dqd[:, off].abs().max()) == 0.0
+    gqdd = g.qdd
+    del g
+    qdd = dynamics.forward_dynamics(m, q, qd, tau)
+    assert float(((gqdd - qdd).abs().amax(dim=1) / qdd.abs().amax(dim=1).clamp_min(1e-30)).max()) < TOL[dt]
+    del gqdd
+    tau2 = dynamics.rnea(m, q, qd, qdd)
+    c = dynamics.bias_force(m, q, qd)
+    scale = tau.abs().amax(dim=1) + c.abs().amax(dim=1)
+    assert float(((tau2 - tau).abs().amax(dim=1) / scale).max()) < TOL[dt], (name, dt, N)
+    del tau2, c, qdd
+    Mi = dynamics.minv_direct(m, q)
+    assert float((Mi - Mi.transpose(1, 2)).abs().max()) <= (1e-12 if dt == "f64" else 1e-5) * float(Mi.abs().max())
 
 
 @pytest.mark.parametrize("pinned", [False, True])

@@ -101,3 +101,26 @@ def test_reference_ir_compiled_for_b200(name, alg):
     torch.cuda.synchronize()
     for (nm, _), o in zip(codegen.outputs(alg, m.n_dof), outs):
         assert rel_err(o.cpu().numpy(), tile(g[f"{alg}.{nm}"])) < 1e-9, (name, alg, nm)
+
+
+@pytest.mark.parametrize("mutate,match", [
+    (lambda t: "\n".join(l for l in t.splitlines() if not l.startswith(("phase", "item", "  "))), "no phases"),
+    (lambda t: t.replace("\narena ", "\narena 1 #", 1), "outside arena"),
+])
+def test_load_text_validates_like_reference(mutate, match):
+    """ir.py:79-99: empty phase lists and out-of-arena segments/slots raise."""
+    bad = mutate(_text("tree7", "FD"))
+    with pytest.raises(kdump.KernelFormatError, match=match):
+        kdump.load_text(bad)
+
+
+def test_load_text_rejects_out_of_range_slot():
+    text = _text("tree7", "FD")
+    arena = int(next(l for l in text.splitlines() if l.startswith("arena")).split()[1])
+    lines = text.splitlines()
+    k = next(i for i, l in enumerate(lines) if l.startswith("  add") or l.startswith("  mul"))
+    parts = lines[k].split()
+    parts[1] = str(arena + 5)
+    lines[k] = "  " + " ".join(parts)
+    with pytest.raises(kdump.KernelFormatError, match="outside arena"):
+        kdump.load_text("\n".join(lines))
