@@ -755,6 +755,9 @@ TUNING_DEFAULT = {
     "ra_budget": 0,      # thread + ra: cap on values kept in registers (0: from the register cap)
     "prefetch_dist": 0,  # thread + ra: issue reloads up to this many ops before use (0: at use)
     "prefetch_slack": 0,  # ... with at most this many prefetched values in flight
+    "fs_warps": 8,       # fs: warps per CTA of the fine-grained schedule
+    "fs_variants": 4,    # fs: column variants of a gradient program (CTA rows)
+    "fs_max_n": 0,       # fs: batch size up to which the fine-grained kernel runs (with "fs" in maps)
 }
 TUNED = {}
 # measured on B200 (N = 2^20): chain7 gradFD fp64 is compute-bound at 6 warps/SM
@@ -763,6 +766,10 @@ TUNED[("chain7", "gradFD", "f64")] = {"park": False, "bk": 32}
 # 32-knot CTAs: finer-grained CTA turnover (staging / write-back barriers),
 # measured 1.35 -> 1.22 ms (fp64) and 0.64 -> 0.60 ms (fp32) at N = 2^20
 TUNED[("chain7", "gradFD", "f32")] = {"bk": 32}
+for _a in ALGORITHMS:
+    for _d in DTYPES:
+        # small batches: the fine-grained warp-specialised schedule (fsched.py)
+        TUNED.setdefault(("chain7", _a, _d), {}).update({"maps": ["thread", "ws", "fs"], "fs_max_n": 1024})
 for _a in ALGORITHMS:
     for _d in DTYPES:
         # measured on B200: with outputs parked in the row, quad12's
@@ -797,7 +804,7 @@ def tuning(model=None, alg=None, dtype=None):
 def _generator_sources():
     here = os.path.dirname(os.path.abspath(__file__))
     h = hashlib.sha256()
-    for f in ("codegen.py", "wsched.py", os.path.join("csrc", "rbd_runtime.cuh")):
+    for f in ("codegen.py", "wsched.py", "fsched.py", os.path.join("csrc", "rbd_runtime.cuh")):
         with open(os.path.join(here, f), "rb") as fh:
             h.update(fh.read())
     return h.hexdigest()
@@ -1589,6 +1596,83 @@ def _ws_struct(model, alg, dt, warps, name=None, trees=None, zero_fill=True, fex
     return "\n".join(src), em.flops, L
 
 
+def _fs_struct(model, alg, dt, warps, variants, name, fext=False, em=None):
+    """Device header of the fine-grained warp-specialised mapping (fsched.py):
+    per (column variant, warp) one asm block holding that warp's whole
+    program, phases separated by bar.sync; arena in shared memory."""
+    from . import fsched
+    if em is None:
+        em = generate_knot(model, alg, dt, fext=fext)
+    n = model.n_dof
+    es = 8 if dt == "f64" else 4
+    nsc = sum(1 for op in em.ops if op[0] == "sincos")
+    sin = em.in_total + 2 * nsc
+    ext = [e for _, e in outputs(alg, n)]
+    ext += [0] * (3 - len(ext))
+    progs = fsched.split_variants(em, variants) if alg in ("gradID", "gradFD") else [em]
+    stage = len(progs) == 1 and 33 * es * (sin + sum(ext)) <= 96 * 1024
+    budget = (FS_SMEM_BUDGET // (33 * es)) - sin - (sum(ext) if stage else 0)
+    scheds = [fsched.FineSchedule(p, warps, max_slots=budget) for p in progs]
+    na = max(1, max(S.nslots for S in scheds))
+    if na > budget:
+        raise GenerationError(f"{model.name} {alg} {dt}: fs arena of {na} slots does not fit shared memory")
+    out_space = "shared" if stage else "global"
+    T = "double" if dt == "f64" else "float"
+    OT = "unsigned" if stage else "unsigned long long"
+    oc = '"r"' if stage else '"l"'
+    K = name
+    ctab = ConstTable(f"rbd_c_{K}", dt)
+    src = [
+        f"// GENERATED by paper_2109_06976_b200.codegen -- robot {model.name!r}, {alg} {dt}, fine-grained "
+        f"warp-specialised ({warps} warps, {len(progs)} column variants)",
+    ]
+    for v, S in enumerate(scheds):
+        src.append(f"// variant {v}: {S.total()} ops in {S.nphases} phases, {S.nslots} arena slots, "
+                   f"simulated {S.critical_path()} cycles (delta {S.delta}, window {S.window})")
+    src += ["#pragma once", '#include "rbd_runtime.cuh"', "@CTAB@",
+            f"struct {K} {{",
+            f"  typedef {T} T;",
+            "  static constexpr int MAP = 2;  // fine-grained warp-specialised: CTA = 32 knots x W warps",
+            f"  static constexpr int W = {warps}, NVAR = {len(progs)}, NDOF = {n}, NIN = {len(em.in_layout)}, "
+            f"NSC = {nsc};",
+            f"  static constexpr int LO = {em.lo}, NP = {em.np};  // input dof window [LO, LO + NP)",
+            ] + _input_consts(em.in_layout) + [
+            f"  static constexpr int E0 = {ext[0]}, E1 = {ext[1]}, E2 = {ext[2]};",
+            f"  static constexpr int SIN = {sin}, NA = {na}, SOUT = {sum(ext)};",
+            f"  static constexpr bool STAGE = {'true' if stage else 'false'};",
+            f"  static constexpr int FLOPS = {em.flops};",
+            "  static constexpr int MINB = 1;",
+            f"  typedef {OT} out_t;",
+            "  __device__ __forceinline__ static void prologue(T* s_in, int warp, int lane) {"]
+    k = 0
+    for op in em.ops:
+        if op[0] == "sincos":
+            slot = op[3]
+            src.append(f"    if (warp == {k % warps}) {{ T s, c; rbd_sincos(s_in[{slot * 33} + lane], &s, &c); "
+                       f"s_in[{(em.in_total + 2 * k) * 33} + lane] = s; s_in[{(em.in_total + 2 * k + 1) * 33} + lane] = c; }}")
+            k += 1
+    src += ["    (void)s_in; (void)warp; (void)lane;", "  }",
+            "  __device__ __forceinline__ static void run(int var, int warp, unsigned a_in, unsigned a_ar, "
+            "out_t a0, out_t a1, out_t a2, unsigned valid) {",
+            f"    switch (var * {warps} + warp) {{"]
+    for v, S in enumerate(scheds):
+        for w in range(warps):
+            body = fsched.ptx_warp(S, w, dt, em.in_total, out_space, ctab,
+                                   sincos_slots=[op[3] for op in em.ops if op[0] == "sincos"])
+            src.append(f"    case {v * warps + w}:  // variant {v}, warp {w}")
+            src.append('      asm volatile("{\\n\\t"')
+            for ln in body:
+                src.append(f'        "{ln}\\n\\t"')
+            src.append(f'        "}}" :: "r"(a_in), "r"(a_ar), {oc}(a0), {oc}(a1), {oc}(a2), "r"(valid) : "memory");')
+            src.append("      break;")
+    src += ["    default: break;", "    }", "  }", "};", ""]
+    text = "\n".join(src).replace("@CTAB@", "\n".join(ctab.declaration()))
+    return text, em.flops, dict(nin=len(em.in_layout), ext=ext)
+
+
+FS_SMEM_BUDGET = 200 * 1024  # dynamic shared memory per CTA the fs mapping may use
+
+
 def mapping(model, alg, dt):
     """'thread' (one knot per thread) or 'ws' (warp-specialised), from tuning."""
     return tuning(model, alg, dt).get("map", "thread")
@@ -1707,9 +1791,12 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
                 X = "X" if fx else ""
                 tags = []
                 for mp in maps:
-                    tag = ("W" if mp == "ws" else "T") + X
+                    tag = {"ws": "W", "fs": "F"}.get(mp, "T") + X
                     K = f"Knot_{alg}_{dt}_{tag}"
-                    if mp == "ws":
+                    if mp == "fs":
+                        text, fl, L = _fs_struct(model, alg, dt, int(tn["fs_warps"]), int(tn["fs_variants"]), K,
+                                                 fext=fx)
+                    elif mp == "ws":
                         text, fl, L = _ws_struct(model, alg, dt, int(tn["warps"]), K, fext=fx)
                     else:
                         text, fl, L = _knot_struct(model, alg, dt, K, fext=fx)
@@ -1771,6 +1858,9 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
                     pick = big
                 else:
                     pick = f"rbd__launch_{alg}_{dt}_{'W' if maps[0] == 'ws' else 'T'}{X}{args}"
+                if "fs" in maps:
+                    # small batches: the fine-grained schedule (lowest latency)
+                    pick = f"N <= {int(tn['fs_max_n'])} ? rbd__launch_{alg}_{dt}_F{X}{args} : ({pick})"
                 dispatch += [
                     f'extern "C" int rbd__launch_{alg}_{dt}{"_fext" if fx else ""}(const void* q, const void* qd, '
                     "const void* u, const void* fx,",

@@ -312,9 +312,106 @@ rbd_ws_kernel(const typename K::T* __restrict__ q, const typename K::T* __restri
   }
 }
 
+// ---------------------------------------------------------------------------
+// fine-grained warp-specialised kernel (fsched.py): CTA = W warps on a group
+// of 32 knots (lane = knot); warp w runs ONE straight-line block holding its
+// share of the op-level list schedule, phases separated by `bar.sync 1`, its
+// values in registers across phases; values another warp reads go through a
+// [slot][33] shared-memory arena.  blockIdx.y = column variant (a gradient
+// program's prefix + one share of its columns).  Persistent over groups.
+// ---------------------------------------------------------------------------
+template <class K>
+__global__ void __launch_bounds__(K::W * 32, K::MINB)
+rbd_fs_kernel(const typename K::T* __restrict__ q, const typename K::T* __restrict__ qd,
+              const typename K::T* __restrict__ u, const typename K::T* __restrict__ fx,
+              typename K::T* __restrict__ o0, typename K::T* __restrict__ o1,
+              typename K::T* __restrict__ o2, long long N) {
+  typedef typename K::T T;
+  constexpr int NT = K::W * 32, L = RBD_WS_LANES;
+  extern __shared__ __align__(16) unsigned char rbd_smem[];
+  T* s_in = reinterpret_cast<T*>(rbd_smem);  // [SIN][33]
+  T* s_ar = s_in + K::SIN * L;                // [NA][33]
+  T* s_out = s_ar + K::NA * L;                // [SOUT][33] when STAGE
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int var = blockIdx.y;
+  const long long groups = (N + 31) / 32;
+  for (long long g = blockIdx.x; g < groups; g += gridDim.x) {
+    const long long base = g * 32;
+    const int nk = (N - base) < 32 ? (int)(N - base) : 32;
+    constexpr int WMAX = 6 * K::NP;
+    constexpr int PMAX = (32 * WMAX + NT - 1) / NT;
+    T v[K::NIN][PMAX];
+#pragma unroll
+    for (int a = 0; a < K::NIN; ++a) {
+      const T* src = (a == 0 ? q : (a == 1 ? qd : (a == 2 ? u : fx))) + base * K::ins(a) + K::ing(a);
+#pragma unroll
+      for (int r = 0; r < (32 * K::inw(a) + NT - 1) / NT; ++r) {
+        const int idx = tid + r * NT;
+        const int k = idx / K::inw(a), j = idx - k * K::inw(a);
+        v[a][r] = (idx < nk * K::inw(a)) ? __ldg(src + k * K::ins(a) + j) : T(0);
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < K::NIN; ++a) {
+#pragma unroll
+      for (int r = 0; r < (32 * K::inw(a) + NT - 1) / NT; ++r) {
+        const int idx = tid + r * NT;
+        if (idx < 32 * K::inw(a)) {
+          const int k = idx / K::inw(a), j = idx - k * K::inw(a);
+          s_in[(K::inr(a) + j) * L + k] = v[a][r];
+        }
+      }
+    }
+    __syncthreads();
+    K::prologue(s_in, warp, lane);
+    __syncthreads();
+    const unsigned a_in = (unsigned)__cvta_generic_to_shared(s_in + lane);
+    const unsigned a_ar = (unsigned)__cvta_generic_to_shared(s_ar + lane);
+    typename K::out_t a0, a1, a2;
+    const int kk = lane < nk ? lane : 0;
+    if constexpr (K::STAGE) {
+      a0 = (unsigned)__cvta_generic_to_shared(s_out + lane);
+      a1 = (unsigned)__cvta_generic_to_shared(s_out + K::E0 * L + lane);
+      a2 = (unsigned)__cvta_generic_to_shared(s_out + (K::E0 + K::E1) * L + lane);
+    } else {
+      a0 = (unsigned long long)(o0 + (base + kk) * K::E0);
+      a1 = (unsigned long long)(K::E1 ? o1 + (base + kk) * K::E1 : o0);
+      a2 = (unsigned long long)(K::E2 ? o2 + (base + kk) * K::E2 : o0);
+    }
+    K::run(var, warp, a_in, a_ar, a0, a1, a2, lane < nk ? 1u : 0u);
+    __syncthreads();
+    if constexpr (K::STAGE) {
+      {
+        T* dst = o0 + base * K::E0;
+        for (int idx = tid; idx < nk * K::E0; idx += NT) {
+          const int k = idx / K::E0, e = idx - k * K::E0;
+          __stcs(dst + idx, s_out[e * L + k]);
+        }
+      }
+      if constexpr (K::E1 > 0) {
+        T* dst = o1 + base * K::E1;
+        for (int idx = tid; idx < nk * K::E1; idx += NT) {
+          const int k = idx / K::E1, e = idx - k * K::E1;
+          __stcs(dst + idx, s_out[(K::E0 + e) * L + k]);
+        }
+      }
+      if constexpr (K::E2 > 0) {
+        T* dst = o2 + base * K::E2;
+        for (int idx = tid; idx < nk * K::E2; idx += NT) {
+          const int k = idx / K::E2, e = idx - k * K::E2;
+          __stcs(dst + idx, s_out[(K::E0 + K::E1 + e) * L + k]);
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 template <class K>
 constexpr size_t rbd_smem_bytes() {
-  if constexpr (K::MAP == 1)
+  if constexpr (K::MAP == 2)
+    return sizeof(typename K::T) * (size_t)RBD_WS_LANES * (K::SIN + K::NA + (K::STAGE ? K::SOUT : 0));
+  else if constexpr (K::MAP == 1)
     return sizeof(typename K::T) * (size_t)RBD_WS_LANES *
            (K::SIN + (K::ARENA_SMEM ? K::NA : 0) + (K::STAGE ? K::SOUT : 0));
   else
@@ -364,11 +461,21 @@ static int rbd_launch_kernel(const void* q, const void* qd, const void* u, const
     cudaError_t e = cudaSuccess;
     // the large-shared-memory opt-in is per device
     if (smem > 48 * 1024) {
-      if constexpr (K::MAP == 1)
+      if constexpr (K::MAP == 2)
+        e = cudaFuncSetAttribute(rbd_fs_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      else if constexpr (K::MAP == 1)
         e = cudaFuncSetAttribute(rbd_ws_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       else
         e = cudaFuncSetAttribute(rbd_batch_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return (int)e;
+    }
+    if constexpr (K::MAP == 2) {
+      int per_sm = 0, sms = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rbd_fs_kernel<K>, K::W * 32, smem);
+      if (e != cudaSuccess) return (int)e;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      // CTAs per variant row: the grid has NVAR rows of them
+      c.grid = ((per_sm > 0 ? per_sm : 1) * sms + K::NVAR - 1) / K::NVAR;
     }
     if constexpr (K::MAP == 1) {
       int per_sm = 0, sms = 0;
@@ -385,7 +492,14 @@ static int rbd_launch_kernel(const void* q, const void* qd, const void* u, const
     }
     c.ready = true;
   }
-  if constexpr (K::MAP == 1) {
+  if constexpr (K::MAP == 2) {
+    guard.unlock();
+    const long long groups = (N + 31) / 32;
+    const long long grid = groups < c.grid ? groups : c.grid;
+    rbd_fs_kernel<K><<<dim3((unsigned)grid, K::NVAR), K::W * 32, smem, (cudaStream_t)stream>>>(
+        (const T*)q, (const T*)qd, (const T*)u, (const T*)fx, (T*)o0, (T*)o1, (T*)o2, (long long)N);
+    return (int)cudaGetLastError();
+  } else if constexpr (K::MAP == 1) {
     const long long groups = (N + 31) / 32;
     const long long grid = groups < c.grid ? groups : c.grid;
     if (K::ARENA_GROUP && !xs) return RBD_EINVAL;

@@ -27,11 +27,12 @@ def _val(tok, regs, f32):
     return regs[tok]
 
 
-def run_block(lines, regions, strides, valid=1, f32=False, consts=None):
+def run_block(lines, regions, strides, valid=1, f32=False, consts=None, regs=None):
     """lines: PTX lines (with '%%' escapes as emitted); regions[k]: dict or
-    array indexed by element; strides[k]: bytes per element step of operand k."""
+    array indexed by element; strides[k]: bytes per element step of operand k.
+    regs: register file to continue from (a warp's block split at barriers)."""
     rnd = (lambda x: float(np.float32(x))) if f32 else (lambda x: x)
-    regs = {}
+    regs = {} if regs is None else regs
     for raw in lines:
         ln = raw.replace("%%", "%").strip().rstrip(";")
         if not ln or ln.startswith(".reg") or ln.startswith("setp") or ln.startswith("bar.sync"):
@@ -79,3 +80,14 @@ def run_block(lines, regions, strides, valid=1, f32=False, consts=None):
             raise ValueError(f"unknown PTX op {op}")
         regs[d] = rnd(r)
     return regs
+
+
+def split_barriers(lines):
+    """A warp's block (fsched.ptx_warp) cut at its `bar.sync 1` lines."""
+    parts = [[]]
+    for ln in lines:
+        if ln.strip() == "bar.sync 1;":
+            parts.append([])
+        else:
+            parts[-1].append(ln)
+    return parts

@@ -332,3 +332,56 @@ def test_split_prefix_and_columns(name, trees, alg):
             got = np.array([o.get(i, np.nan) for i in idx])
             assert np.all(np.isfinite(got)), (name, alg, nm)
             assert rel_err(got[None], ref[idx][None]) < 1e-12, (name, alg, nm)
+
+
+def run_fs(model, alg, dt, x, warps, variants, fext=False):
+    """The fine-grained mapping (fsched): every (variant, warp) block of the
+    exact device PTX, warps interleaved phase by phase (each warp's
+    registers persist across its barriers), arena shared by the variant's
+    warps; outputs merged over the variants."""
+    from paper_2109_06976_b200 import fsched
+    em = codegen.generate_knot(model, alg, dt, fext=fext)
+    n = model.n_dof
+    es = 8 if dt == "f64" else 4
+    L = 33
+    row = {i: float(v) for i, v in enumerate(x)}
+    for k, slot in enumerate(_sincos_slots(em)):
+        row[em.in_total + 2 * k] = math.sin(x[slot])
+        row[em.in_total + 2 * k + 1] = math.cos(x[slot])
+    outs = [dict() for _ in range(3)]
+    progs = fsched.split_variants(em, variants) if alg in ("gradID", "gradFD") else [em]
+    scheds = []
+    for p in progs:
+        S = fsched.FineSchedule(p, warps)
+        scheds.append(S)
+        ctab = codegen.ConstTable("K", dt)
+        scs = [op[3] for op in em.ops if op[0] == "sincos"]
+        parts = [ptxsim.split_barriers(fsched.ptx_warp(S, w, dt, em.in_total, "global", ctab, sincos_slots=scs))
+                 for w in range(warps)]
+        assert all(len(pp) == S.nphases for pp in parts)
+        arena = {}
+        regs = [dict() for _ in range(warps)]
+        consts = {"K": sorted(ctab.index, key=ctab.index.get)}
+        for ph in range(S.nphases):
+            for w in range(warps):
+                ptxsim.run_block(parts[w][ph], [row, arena] + outs + [None], [L * es, L * es, es, es, es],
+                                 f32=(dt == "f32"), consts=consts, regs=regs[w])
+    return [np.array([o.get(i, np.nan) for i in range(e)]) for o, (_, e) in zip(outs, codegen.outputs(alg, n))], scheds
+
+
+@pytest.mark.parametrize("name", ["pendulum2", "chain7", "tree7", "mixed5", "quad12"])
+@pytest.mark.parametrize("alg", ["ID", "Minv", "FD", "gradID", "gradFD"])
+def test_fs_schedule_matches_reference(name, alg):
+    """Fine-grained schedule (fsched): 8 warps, 3 column variants for the
+    gradients -- every variant's blocks run phase by phase against the
+    reference outputs; warps read other warps' values only from the arena."""
+    g = golden(name)
+    m = models.load(name)
+    n = m.n_dof
+    k = 1
+    x = _inputs(g, alg, k, n)
+    got, scheds = run_fs(m, alg, "f64", x, 8, 3)
+    for (nm, _), v in zip(codegen.outputs(alg, n), got):
+        ref = g[f"{alg}.{nm}"][k]
+        assert np.all(np.isfinite(v)), (name, alg, nm)
+        assert rel_err(v[None], ref[None]) < 1e-12, (name, alg, nm)
