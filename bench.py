@@ -5,7 +5,8 @@ Headline workload (BASELINE.json configs[4], the large-batch single-GPU case
 of the metric): iiwa stand-in `chain7`, gradFD (dFD = -Minv dID, plus qdd),
 fp64 (the reference precision), N = 1,048,576 knot points per GPU, synthetic
 seeded states.  Weak scaling: every rank evaluates its own N
-knots (knots are independent; no data-path collective).
+knots (knots are independent; no data-path collective); under N>1 ranks the
+line also carries `strong` (one N-knot batch sliced ceil(N/G) per rank).
 
   value  knots/s, kernel only: inputs resident in HBM, one launch of the
          generated batch kernel per step, CUDA events on the launch stream,
@@ -13,20 +14,27 @@ knots (knots are independent; no data-path collective).
          126 MB L2, so no flush is needed between steps.
   e2e    knots/s through the C ABI's host-buffer entry (rbd_run_host):
          pinned host inputs -> H2D -> kernel -> D2H -> pinned host outputs,
-         all inside the timed region, pipelined over the session's streams.
+         all inside the timed region, pipelined over the session's streams;
+         `e2e.dropin` times the reference-named drop-in call
+         (dynamics.fd_grad on numpy arrays) the same way.
   roofline  fp64 CUDA-core FMA roofline: achieved = reference-IR flops per
          knot (BASELINE.md §3: 17,131 for chain7 gradFD) x N / kernel time;
          peak = fp64 FMA throughput measured in this run (rbd_peak.cu), since
          MEASURED_PEAKS.json holds only HBM and bf16-tensor peaks.
-  cpu_baseline  the oracle port of the reference CPU path
-         (oracle/refdyn_np.py = rbdgen.refdyn restated) on the host cores,
-         bounded sample, multiprocessing pool.
-  sweep  the other BASELINE configs (iiwa N=16..256 fp32/fp64 kernel-only and
-         with I/O incl. the "us per N=128 batch w/ I/O" headline, HyQ N=128,
-         Atlas N=256, Atlas 1M) -- reported, not the headline.
+  cpu_baseline  the reference itself (rbdgen.refdyn, installed under
+         baseline/_ref) on the host cores, bounded sample, process pool;
+         `secondary` = rbdgen.interp over codegen.build's program.
+  small_batch  BASELINE configs 1-4 as top-level numbers: device time per
+         launch (CUDA-graph replay: no host launch overhead), the per-call
+         latency with host I/O through the C ABI and through the Python
+         drop-in, for iiwa N=128 (all algorithms), HyQ N=128, Atlas N=256.
+  sweep  every config point (iiwa N=16..256 fp32/fp64, large-batch
+         iiwa/HyQ/Atlas up to 1M, rollouts) with per-point roofline fractions.
 
-`--impl reference` times the reference's CPU implementation (the oracle port;
-the Python reference cannot travel to the GPU box) on the same workload.
+`--impl reference` times the reference's CPU implementation (rbdgen.refdyn
+from baseline/_ref; the oracle port only if that install is absent) on the
+same workload.  `--gpus N` without torchrun re-launches itself under
+torch.distributed.run with N ranks.
 """
 
 import argparse
@@ -38,10 +46,13 @@ import sys
 import threading
 import time
 
-import numpy as np
+os.environ.setdefault("OMP_NUM_THREADS", "1")  # the CPU baseline's numpy: one thread per process
+
+import numpy as np  # noqa: E402
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 REF_IR_FLOPS = {  # BASELINE.md §3, counted on the reference's generated IR (FMA = 2)
     ("chain7", "ID"): 1091, ("chain7", "Minv"): 4244, ("chain7", "FD"): 5341,
@@ -52,6 +63,7 @@ REF_IR_FLOPS = {  # BASELINE.md §3, counted on the reference's generated IR (FM
     ("humanoid30", "gradID"): 57839, ("humanoid30", "gradFD"): 96220,
 }
 PAPER = {"chain7": "iiwa", "quad12": "HyQ", "humanoid30": "Atlas"}
+N_IN = {"ID": 3, "Minv": 1, "FD": 3, "gradID": 3, "gradFD": 3}
 
 
 def states(n, N, seed=1, dtype=np.float64):
@@ -62,34 +74,97 @@ def states(n, N, seed=1, dtype=np.float64):
     return [x.astype(dtype) for x in (q, qd, u)]
 
 
+def io_scalars(alg, n):
+    outs = {"ID": n, "Minv": n * n, "FD": n, "gradID": 2 * n * n, "gradFD": 2 * n * n + n}[alg]
+    return N_IN[alg] * n, outs
+
+
 # ---------------------------------------------------------------------------
-# CPU reference path (oracle port), multiprocessing over host cores
+# CPU reference path: the reference package itself (baseline/_ref/rbdgen),
+# multiprocessing over host cores (processes: the GIL serialises threads)
 # ---------------------------------------------------------------------------
 
+def reference_available():
+    return os.path.isdir(os.path.join(REF_DIR, "rbdgen"))
+
+
+_W = {}
+
+
+def _cpu_setup(robot, alg, impl):
+    key = (robot, alg, impl)
+    if key in _W:
+        return _W[key]
+    if impl in ("refdyn", "interp"):
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        from rbdgen import models as RM
+        from rbdgen import refdyn
+        m = RM.load(robot)
+        if impl == "refdyn":
+            fn = {"ID": lambda q, qd, u: refdyn.rnea(m, q, qd, u),
+                  "Minv": lambda q, qd, u: refdyn.minv_direct(m, q),
+                  "FD": lambda q, qd, u: refdyn.forward_dynamics(m, q, qd, u),
+                  "gradID": lambda q, qd, u: refdyn.rnea_grad(m, q, qd, u),
+                  "gradFD": lambda q, qd, u: refdyn.fd_grad(m, q, qd, u)}[alg]
+        else:
+            from rbdgen import codegen as RC
+            from rbdgen import interp
+            prog = RC.build(m, alg)[0]
+            names = {"ID": ("q", "qd", "qdd"), "Minv": ("q",), "FD": ("q", "qd", "tau"),
+                     "gradID": ("q", "qd", "qdd"), "gradFD": ("q", "qd", "tau")}[alg]
+
+            def fn(q, qd, u, prog=prog, names=names):
+                return interp.interpret(prog, dict(zip(names, (q, qd, u))), thread_count=1)
+    else:  # "port": the oracle restatement (used only when baseline/_ref is absent)
+        from oracle import refdyn_np as R
+        from paper_2109_06976_b200 import models
+        m = models.load(robot)
+
+        def fn(q, qd, u):
+            return R.evaluate(m, alg, q, qd, u)
+    _W[key] = fn
+    return fn
+
+
 def _cpu_worker(args):
-    robot, alg, q, qd, u = args
-    sys.path.insert(0, ROOT)
-    from oracle import refdyn_np as R
-    from paper_2109_06976_b200 import models
-    m = models.load(robot)
+    robot, alg, impl, q, qd, u = args
+    fn = _cpu_setup(robot, alg, impl)
     for k in range(q.shape[0]):
-        R.evaluate(m, alg, q[k], qd[k], u[k])
+        fn(q[k], qd[k], u[k])
     return q.shape[0]
 
 
-def cpu_reference_rate(robot, alg, sample, cores):
-    """knots/s of the reference CPU path on `sample` knots over `cores` processes."""
+def cpu_impl_default():
+    return "refdyn" if reference_available() else "port"
+
+
+def cpu_reference_rate(robot, alg, impl, cores, seconds=12.0, max_sample=65536, pool=None):
+    """(knots/s, sample knots, wall s) of the CPU path over `cores` processes,
+    sample sized for ~`seconds` of wall time (calibrated on one process)."""
     from paper_2109_06976_b200 import models
     n = models.load(robot).n_dof
-    q, qd, u = states(n, sample, seed=1)
-    chunks = [(robot, alg, q[i::cores], qd[i::cores], u[i::cores]) for i in range(cores)]
-    ctx = mp.get_context("fork")
-    with ctx.Pool(cores) as pool:
-        pool.map(_cpu_worker, [(robot, alg, q[:1], qd[:1], u[:1])] * cores)  # warm (imports, parse)
+    own = pool is None
+    if own:
+        pool = mp.get_context("fork").Pool(cores)
+    try:
+        q, qd, u = states(n, 4 * cores, seed=1)
+        pool.map(_cpu_worker, [(robot, alg, impl, q[i:i + 1], qd[i:i + 1], u[i:i + 1]) for i in range(cores)])
+        _cpu_worker((robot, alg, impl, q[:1], qd[:1], u[:1]))  # setup (model parse, codegen.build) untimed
+        t0 = time.perf_counter()
+        _cpu_worker((robot, alg, impl, q[:3], qd[:3], u[:3]))
+        per_knot = (time.perf_counter() - t0) / 3
+        sample = int(min(max_sample, max(cores, seconds / max(per_knot, 1e-9) * cores)))
+        q, qd, u = states(n, sample, seed=1)
+        chunks = [(robot, alg, impl, q[i::cores], qd[i::cores], u[i::cores]) for i in range(cores)]
         t0 = time.perf_counter()
         done = sum(pool.map(_cpu_worker, chunks))
         dt = time.perf_counter() - t0
-    return done / dt, dt
+    finally:
+        if own:
+            pool.close()
+            pool.join()
+    return done / dt, sample, dt
 
 
 def host_cores():
@@ -109,8 +184,28 @@ def cpu_model():
     return "unknown"
 
 
+def cpu_baseline(robot, alg, cores, seconds=12.0):
+    """The reference CPU path (primary refdyn, secondary interp) on this host."""
+    impl = cpu_impl_default()
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        rate, sample, secs = cpu_reference_rate(robot, alg, impl, cores, seconds, pool=pool)
+        rec = {"value": rate, "unit": "knots/s", "cores": cores,
+               "kind": "reference" if impl == "refdyn" else "port",
+               "impl": ("rbdgen.refdyn (baseline/_ref, the unmodified reference)" if impl == "refdyn"
+                        else "oracle/refdyn_np.py (port; baseline/_ref absent)"),
+               "sample": f"{sample} knots of {robot} {alg} f64 (seed 1), {secs:.1f} s wall over {cores} processes, "
+                         "OMP_NUM_THREADS=1",
+               "cpu": cpu_model()}
+        if impl == "refdyn":
+            r2, s2, t2 = cpu_reference_rate(robot, alg, "interp", cores, seconds / 2, pool=pool)
+            rec["secondary"] = {"value": r2, "unit": "knots/s", "impl": "rbdgen.interp.interpret(codegen.build(...))",
+                                "sample": f"{s2} knots, {t2:.1f} s wall over {cores} processes"}
+    return rec
+
+
 # ---------------------------------------------------------------------------
-# clocks sampler (nvidia-smi during the timed region)
+# clocks sampler (NVML during the timed region)
 # ---------------------------------------------------------------------------
 
 class Clocks:
@@ -185,7 +280,7 @@ def fma_peak_tflops(torch, dtype):
     lib = kernels.peak_library()
     sink = torch.empty(256, dtype=torch.float64, device="cuda")
     st = torch.cuda.current_stream()
-    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
     blocks, iters = sms * 8, 4096
     per_iter = 2 * 16
     for _ in range(3):
@@ -201,17 +296,22 @@ def fma_peak_tflops(torch, dtype):
     return best
 
 
-def device_rate(torch, lib, robot, alg, dt, N, steps, warmup, stream):
-    """Kernel-only: ms per launch (CUDA events on the launch stream)."""
-    from paper_2109_06976_b200 import codegen, models, runtime
+def _device_buffers(torch, robot, alg, dt, N, begin=0, total=None):
+    from paper_2109_06976_b200 import codegen, models
     m = models.load(robot)
     n = m.n_dof
     tdt = torch.float64 if dt == "f64" else torch.float32
-    xs = [torch.from_numpy(x).to("cuda", tdt) for x in states(n, N, seed=1)]
-    nin = len(codegen.INPUTS[alg])
+    total = N if total is None else total
+    xs = [torch.from_numpy(x[begin:begin + N]).to("cuda", tdt) for x in states(n, total, seed=1)]
     outs = [torch.empty((N, e), dtype=tdt, device="cuda") for _, e in codegen.outputs(alg, n)]
-    ins = [x.data_ptr() for x in xs[:nin]]
-    ops = [o.data_ptr() for o in outs]
+    return [x.data_ptr() for x in xs[:N_IN[alg]]], [o.data_ptr() for o in outs], (xs, outs)
+
+
+def device_rate(torch, lib, robot, alg, dt, N, steps, warmup, stream, begin=0, total=None):
+    """Kernel-only: ms per launch (CUDA events on the launch stream), launches
+    issued back to back from the host."""
+    from paper_2109_06976_b200 import runtime
+    ins, ops, keep = _device_buffers(torch, robot, alg, dt, N, begin, total)
     with torch.cuda.stream(stream):
         for _ in range(warmup):
             runtime.launch(lib, alg, dt, ins, ops, N, stream.cuda_stream)
@@ -222,16 +322,47 @@ def device_rate(torch, lib, robot, alg, dt, N, steps, warmup, stream):
             runtime.launch(lib, alg, dt, ins, ops, N, stream.cuda_stream)
         e1.record(stream)
         torch.cuda.synchronize()
+    del keep
     return e0.elapsed_time(e1) / steps
 
 
-def host_rate(torch, lib, robot, alg, dt, N, steps, warmup, reps_floor=1):
-    """End to end through rbd_run_host from pinned host buffers: s per step."""
+def graph_rate(torch, lib, robot, alg, dt, N, reps=50, rounds=5):
+    """Device time per launch (us), from a CUDA graph of `reps` back-to-back
+    launches (no host launch overhead in the number; min over rounds)."""
+    from paper_2109_06976_b200 import runtime
+    ins, ops, keep = _device_buffers(torch, robot, alg, dt, N)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for _ in range(3):
+            runtime.launch(lib, alg, dt, ins, ops, N, st.cuda_stream)
+        st.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for _ in range(reps):
+                runtime.launch(lib, alg, dt, ins, ops, N, st.cuda_stream)
+        g.replay()
+        st.synchronize()
+        best = None
+        for _ in range(rounds):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            g.replay()
+            e1.record(st)
+            e1.synchronize()
+            t = e0.elapsed_time(e1) * 1e3 / reps
+            best = t if best is None else min(best, t)
+    del g, keep
+    return best
+
+
+def host_rate(torch, lib, robot, alg, dt, N, steps, warmup):
+    """End to end through rbd_run_host from pinned host buffers: s per step
+    (Python Session.run), plus the same call timed inside the library."""
     from paper_2109_06976_b200 import codegen, models, runtime
     m = models.load(robot)
     n = m.n_dof
     tdt = torch.float64 if dt == "f64" else torch.float32
-    nin = len(codegen.INPUTS[alg])
+    nin = N_IN[alg]
     pins = [torch.from_numpy(x).to(tdt).pin_memory() for x in states(n, N, seed=1)[:nin]]
     pouts = [torch.empty((N, e), dtype=tdt).pin_memory() for _, e in codegen.outputs(alg, n)]
     ins = [p.numpy() for p in pins]
@@ -244,12 +375,131 @@ def host_rate(torch, lib, robot, alg, dt, N, steps, warmup, reps_floor=1):
         sess.run(alg, dt, ins, outs, N)
     dt_s = (time.perf_counter() - t0) / steps
     es = 8 if dt == "f64" else 4
-    h2d = nin * n * N * es
-    d2h = sum(e for _, e in codegen.outputs(alg, n)) * N * es
-    chunks = -(-N // sess.chunk)
+    si, so = io_scalars(alg, n)
     # the same C-ABI call timed inside the library (no Python/ctypes overhead)
     c_s = sess.bench(alg, dt, ins, outs, N, steps)
-    return dt_s, h2d, d2h, chunks, c_s
+    return dt_s, si * N * es, so * N * es, c_s
+
+
+def dropin_rate(robot, alg, dt, N, steps, warmup):
+    """s per call of the reference-named drop-in (dynamics.<fn>) on numpy
+    arrays: validation, output allocation, H2D, kernel, D2H, reshaping."""
+    from paper_2109_06976_b200 import dynamics, models
+    m = models.load(robot)
+    ndt = np.float64 if dt == "f64" else np.float32
+    q, qd, u = states(m.n_dof, N, seed=1, dtype=ndt)
+    fn = {"ID": lambda: dynamics.rnea(m, q, qd, u), "Minv": lambda: dynamics.minv_direct(m, q),
+          "FD": lambda: dynamics.forward_dynamics(m, q, qd, u), "gradID": lambda: dynamics.rnea_grad(m, q, qd, u),
+          "gradFD": lambda: dynamics.fd_grad(m, q, qd, u)}[alg]
+    for _ in range(warmup):
+        fn()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        r = fn()
+    del r
+    return (time.perf_counter() - t0) / steps
+
+
+def _hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0  # B200_PROFILING.md fallback
+
+
+def point(torch, stream, peaks, robot, alg, dt, N, reps, io=False, graph=False, dropin=False, io_steps=None):
+    """One config point with its roofline fractions."""
+    from paper_2109_06976_b200 import kernels, models
+    lib = kernels.library(models.load(robot))
+    n = models.load(robot).n_dof
+    rec = {"robot": robot, "paper_robot": PAPER.get(robot), "alg": alg, "dtype": dt, "N": N}
+    if graph:
+        us = graph_rate(torch, lib, robot, alg, dt, N)
+        rec["launch_us"] = device_rate(torch, lib, robot, alg, dt, N, reps, 5, stream) * 1e3
+    else:
+        us = device_rate(torch, lib, robot, alg, dt, N, reps, 5, stream) * 1e3
+    rec["kernel_us"] = us
+    rec["kernel_timing"] = "CUDA-graph replay, device time per launch" if graph else "CUDA events, back-to-back launches"
+    rec["kernel_knots_per_s"] = N / (us * 1e-6)
+    fl = REF_IR_FLOPS.get((robot, alg))
+    es = 8 if dt == "f64" else 4
+    si, so = io_scalars(alg, n)
+    if fl:
+        rec["ref_ir_tflops"] = fl * N / (us * 1e-6) / 1e12
+        rec["flops_frac"] = rec["ref_ir_tflops"] / peaks[dt]
+    rec["hbm_frac"] = (si + so) * es * N / (us * 1e-6) / 1e9 / _hbm_peak()
+    if io:
+        steps = io_steps or (max(5, reps // 2) if N <= 4096 else 3)
+        s, h2d, d2h, c_s = host_rate(torch, lib, robot, alg, dt, N, steps, 2)
+        rec.update(io_us=s * 1e6, io_knots_per_s=N / s, io_c_abi_us=c_s * 1e6, io_bytes=h2d + d2h)
+    if dropin:
+        steps = max(5, reps // 2) if N <= 4096 else 3
+        rec["dropin_us"] = dropin_rate(robot, alg, dt, N, steps, 2) * 1e6
+    return rec
+
+
+def small_batch(torch, stream, peaks, reps):
+    """BASELINE configs 1-4: iiwa suite at N=128 (both dtypes), HyQ dFD N=128,
+    Atlas dFD N=256 -- device time, and latency with host I/O."""
+    pts = []
+    for dt in ("f64", "f32"):
+        for alg in ("ID", "Minv", "FD", "gradID", "gradFD"):
+            pts.append(point(torch, stream, peaks, "chain7", alg, dt, 128, reps, io=True, graph=True,
+                             dropin=(alg == "gradFD")))
+        pts.append(point(torch, stream, peaks, "quad12", "gradFD", dt, 128, reps, io=True, graph=True, dropin=True))
+        pts.append(point(torch, stream, peaks, "humanoid30", "gradFD", dt, 256, reps, io=True, graph=True,
+                         dropin=True))
+    head = {}
+    for p in pts:
+        k = f"{p['paper_robot']}_{p['alg']}_{p['dtype']}_N{p['N']}"
+        head[k] = {"kernel_us": round(p["kernel_us"], 2), "io_us_c_abi": round(p["io_c_abi_us"], 2),
+                   "io_us_python": round(p["io_us"], 2)}
+        if "dropin_us" in p:
+            head[k]["io_us_dropin"] = round(p["dropin_us"], 2)
+    return head, pts
+
+
+def sweep(torch, stream, peaks, args):
+    out = []
+    reps = max(args.steps * 10, 50)
+    for dt in ("f64", "f32"):
+        for N in (16, 32, 64, 256):
+            for alg in ("ID", "Minv", "FD", "gradID", "gradFD"):
+                out.append(point(torch, stream, peaks, "chain7", alg, dt, N, reps, io=(alg == "gradFD"), graph=True))
+        out.append(point(torch, stream, peaks, "quad12", "gradFD", dt, 16, reps, io=True, graph=True))
+        out.append(point(torch, stream, peaks, "humanoid30", "gradFD", dt, 16, reps, io=True, graph=True))
+    # device-resident rollouts (rollout.py): B trajectories x H steps of gradFD + Euler, graph-replayed
+    from paper_2109_06976_b200 import models
+    from paper_2109_06976_b200.rollout import Rollout
+    for robot, B, H in (("chain7", 128, 64), ("chain7", 4096, 64), ("humanoid30", 128, 32)):
+        m = models.load(robot)
+        n = m.n_dof
+        r = Rollout(m, B, H, 0.01, "f64", grad=True, graph=True)
+        rng = np.random.default_rng(1)
+        q0 = torch.from_numpy(rng.uniform(-1, 1, (B, n))).cuda()
+        tau = torch.from_numpy(rng.uniform(-1, 1, (B, H, n))).cuda()
+        for _ in range(3):
+            r.run(q0, q0, tau)
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(10):
+            r.run(q0, q0, tau)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 10
+        out.append({"robot": robot, "paper_robot": PAPER.get(robot), "alg": "rollout(gradFD+Euler)", "dtype": "f64",
+                    "N": B * H, "trajectories": B, "horizon": H, "kernel_us": ms * 1e3,
+                    "kernel_knots_per_s": B * H / (ms * 1e-3), "graph": True})
+    # BASELINE configs[4]: large batches (iiwa, HyQ, Atlas up to 1M knots)
+    big = {"chain7": (65536, 262144, 1048576), "quad12": (65536, 1048576), "humanoid30": (65536, 262144, 1048576)}
+    for robot, Ns in big.items():
+        for dt in ("f64", "f32"):
+            for N in Ns:
+                last = N == Ns[-1]
+                out.append(point(torch, stream, peaks, robot, "gradFD", dt, N, max(args.steps // 2, 3), io=last,
+                                 dropin=last and dt == "f64", io_steps=2))
+    return out
 
 
 def run_ours(args):
@@ -261,7 +511,8 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     # RBD_BENCH_SHARED_GPU=1: every rank on cuda:0 with gloo plumbing -- only
-    # to exercise the multi-rank code path on a one-GPU box (not a scaling run)
+    # to exercise the multi-rank code path on a one-GPU box (not a scaling run;
+    # the line then says n_gpus 1 and shared_gpu true)
     shared = os.environ.get("RBD_BENCH_SHARED_GPU") == "1"
     if world > 1:
         torch.cuda.set_device(0 if shared else local)
@@ -292,8 +543,9 @@ def run_ours(args):
 
     peak64 = fma_peak_tflops(torch, "f64")
     peak32 = fma_peak_tflops(torch, "f32")
+    peaks = {"f64": peak64, "f32": peak32}
 
-    # -- headline, kernel only ---------------------------------------------------
+    # -- headline, kernel only (weak: N knots per rank) -----------------------------
     barrier()
     with Clocks(0 if shared else local) as clk:
         ms = device_rate(torch, lib, robot, alg, dt, N, args.steps, args.warmup, stream)
@@ -301,18 +553,33 @@ def run_ours(args):
     ms = max_over_ranks(ms)
     value = N * world / (ms * 1e-3)
 
+    # -- strong scaling: one N-knot batch, ceil(N / world) contiguous knots per rank --
+    strong = None
+    if world > 1:
+        per = -(-N // world)
+        b = min(per * rank, N)
+        mine = max(0, min(b + per, N) - b)
+        barrier()
+        s_ms = device_rate(torch, lib, robot, alg, dt, mine, args.steps, args.warmup, stream, begin=b, total=N) \
+            if mine else 0.0
+        barrier()
+        s_ms = max_over_ranks(s_ms)
+        strong = {"value": N / (s_ms * 1e-3), "unit": "knots/s", "ms_per_step": s_ms, "knots_total": N,
+                  "knots_per_rank": per, "scaling": "strong"}
+
     # -- headline, end to end via the C ABI host path ------------------------------
     barrier()
-    e2e_s, h2d, d2h, chunks, e2e_c = host_rate(torch, lib, robot, alg, dt, N, max(2, args.steps // 4), 1)
+    e2e_steps = max(3, args.steps // 4)
+    e2e_s, h2d, d2h, e2e_c = host_rate(torch, lib, robot, alg, dt, N, e2e_steps, 1)
     barrier()
     e2e_s = max_over_ranks(e2e_s)
     e2e = N * world / e2e_s
+    dropin_s = dropin_rate(robot, alg, dt, N, 2, 1) if rank == 0 else None
 
     flops_ref = REF_IR_FLOPS.get((robot, alg))
     flops_ours = meta["flops_per_knot"].get(f"{alg}_{dt}")
-    peak = peak64 if dt == "f64" else peak32
+    peak = peaks[dt]
     achieved = flops_ref * N / (ms * 1e-3) / 1e12 if flops_ref else None
-    es = 8 if dt == "f64" else 4
     alg_bytes = (h2d + d2h)  # compulsory HBM bytes per launch = inputs + outputs
     traffic, traffic_src = None, None
     # dram__bytes_read+write per launch of this kernel from the newest committed
@@ -320,7 +587,7 @@ def run_ours(args):
     import glob
     import re
     profs = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_summary_r*.json")),
-                   key=lambda f: int(re.search(r"_r(\d+)", f).group(1)))
+                   key=lambda f: (int(re.search(r"_r(\d+)", f).group(1)), f))
     for prof in reversed(profs):
         try:
             t = json.load(open(prof)).get(f"{robot}_{alg}_{dt}", {}).get("dram_bytes_per_launch")
@@ -330,11 +597,12 @@ def run_ours(args):
             traffic, traffic_src = t * N / (1 << 20), os.path.relpath(prof, ROOT)
             break
 
+    n_gpus = 1 if shared else world
     result = {
         "metric": f"dFD knot-points/sec ({PAPER.get(robot, robot)} stand-in {robot}, {alg}, N={N}/GPU)",
         "value": value,
         "unit": "knots/s",
-        "n_gpus": world,
+        "n_gpus": n_gpus,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": ms,
@@ -345,7 +613,7 @@ def run_ours(args):
         "data": "synthetic seeded states q~U(-pi,pi), qd,tau~U(-1,1) (SURVEY 8d, seed 1)",
         "config": {"workload": f"{robot} {alg} {dt}, N={N} knots per GPU, one batched launch per step",
                    "robot": robot, "paper_robot": PAPER.get(robot), "algorithm": alg, "knots_per_gpu": N,
-                   "parallelism": f"batch-sharded x{world}, no collective",
+                   "parallelism": f"batch-sharded x{world}, no collective" + (" (ranks share cuda:0)" if shared else ""),
                    "l2": "inputs+outputs per step exceed the 126 MB L2 (no flush needed)"},
         "e2e": {"value": e2e, "unit": "knots/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_s * 1e3, "path": "Python Session.run -> rbd_run_host (C ABI, pinned host buffers)",
@@ -369,86 +637,27 @@ def run_ours(args):
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
     }
+    if dropin_s is not None:
+        result["e2e"]["dropin"] = {"value": N / dropin_s, "unit": "knots/s", "ms_per_step": dropin_s * 1e3,
+                                   "path": f"dynamics.{'fd_grad' if alg == 'gradFD' else alg}(model, q, qd, tau) "
+                                           "on numpy arrays (reference-named drop-in)"}
+    if shared:
+        result["shared_gpu"] = True
+        result["ranks"] = world
+    if strong:
+        result["strong"] = strong
 
     # -- the other BASELINE configs (rank 0 device, not part of the headline) ------
     if rank == 0 and not args.no_sweep:
-        result["sweep"] = sweep(torch, stream, args)
+        result["small_batch"], pts = small_batch(torch, stream, peaks, max(args.steps * 10, 50))
+        result["sweep"] = pts + sweep(torch, stream, peaks, args)
     if rank == 0:
         if not args.no_cpu:
-            cores = host_cores()
-            sample = args.cpu_sample
-            rate, secs = cpu_reference_rate(robot, alg, sample, cores)
-            result["cpu_baseline"] = {"value": rate, "unit": "knots/s", "cores": cores, "kind": "port",
-                                      "sample": f"{sample} knots of {robot} {alg} (seed 1), "
-                                                f"{secs:.1f} s wall over {cores} processes",
-                                      "cpu": cpu_model()}
+            result["cpu_baseline"] = cpu_baseline(robot, alg, host_cores(), args.cpu_seconds)
         print(json.dumps(result), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
-
-
-def _hbm_peak():
-    try:
-        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
-    except Exception:
-        return 6650.0  # B200_PROFILING.md fallback
-
-
-def sweep(torch, stream, args):
-    from paper_2109_06976_b200 import kernels, models
-    out = []
-    reps = max(args.steps * 10, 50)
-
-    def entry(robot, alg, dt, N, io=True, reps=reps):
-        lib = kernels.library(models.load(robot))
-        ms = device_rate(torch, lib, robot, alg, dt, N, reps, 5, stream)
-        rec = {"robot": robot, "paper_robot": PAPER.get(robot), "alg": alg, "dtype": dt, "N": N,
-               "kernel_us": ms * 1e3, "kernel_knots_per_s": N / (ms * 1e-3)}
-        fl = REF_IR_FLOPS.get((robot, alg))
-        if fl:
-            rec["ref_ir_tflops"] = fl * N / (ms * 1e-3) / 1e12
-        if io:
-            s, h2d, d2h, _, c_s = host_rate(torch, lib, robot, alg, dt, N, max(5, reps // 2) if N <= 4096 else 3, 2)
-            rec.update(io_us=s * 1e6, io_knots_per_s=N / s, io_c_abi_us=c_s * 1e6)
-        out.append(rec)
-
-    for dt in ("f64", "f32"):
-        for N in (16, 32, 64, 128, 256):
-            for alg in ("ID", "Minv", "FD", "gradID", "gradFD"):
-                entry("chain7", alg, dt, N, io=(alg == "gradFD" or N == 128))
-    entry("quad12", "gradFD", "f64", 128)
-    entry("quad12", "gradFD", "f32", 128)
-    entry("humanoid30", "gradFD", "f64", 256)
-    entry("humanoid30", "gradFD", "f32", 256)
-    # device-resident rollouts (rollout.py): B trajectories x H steps of gradFD + Euler, graph-replayed
-    from paper_2109_06976_b200.rollout import Rollout
-    for robot, B, H in (("chain7", 128, 64), ("chain7", 4096, 64), ("humanoid30", 128, 32)):
-        m = models.load(robot)
-        n = m.n_dof
-        r = Rollout(m, B, H, 0.01, "f64", grad=True, graph=True)
-        rng = np.random.default_rng(1)
-        q0 = torch.from_numpy(rng.uniform(-1, 1, (B, n))).cuda()
-        tau = torch.from_numpy(rng.uniform(-1, 1, (B, H, n))).cuda()
-        for _ in range(3):
-            r.run(q0, q0, tau)
-        st = torch.cuda.current_stream()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
-        for _ in range(10):
-            r.run(q0, q0, tau)
-        e1.record(st)
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / 10
-        out.append({"robot": robot, "paper_robot": PAPER.get(robot), "alg": "rollout(gradFD+Euler)", "dtype": "f64",
-                    "N": B * H, "trajectories": B, "horizon": H, "kernel_us": ms * 1e3,
-                    "kernel_knots_per_s": B * H / (ms * 1e-3), "graph": True})
-    for robot in ("chain7", "quad12", "humanoid30"):
-        for dt in ("f64", "f32"):
-            Ns = {"chain7": (65536, 262144, 1048576), "quad12": (1048576,), "humanoid30": (65536, 262144)}[robot]
-            for N in Ns:
-                entry(robot, "gradFD", dt, N, io=(N == Ns[-1]), reps=max(args.steps // 2, 3))
-    return out
 
 
 def run_reference(args):
@@ -456,27 +665,48 @@ def run_reference(args):
     if rank != 0:
         return
     cores = host_cores()
-    sample = max(cores, args.cpu_sample // 4)  # per step: ~3 s of CPU work on 16 cores
-    rates = []
-    for _ in range(args.warmup):
-        cpu_reference_rate(args.robot, args.alg, cores * 4, cores)
-    for _ in range(max(1, args.steps)):
-        rates.append(cpu_reference_rate(args.robot, args.alg, sample, cores)[0])
+    impl = cpu_impl_default()
+    rates, samples = [], []
+    ctx = mp.get_context("fork")
+    per_step = max(2.0, args.cpu_seconds / 4)
+    with ctx.Pool(cores) as pool:
+        for _ in range(args.warmup):
+            cpu_reference_rate(args.robot, args.alg, impl, cores, 0.5, pool=pool)
+        for _ in range(max(1, args.steps)):
+            r, s, _ = cpu_reference_rate(args.robot, args.alg, impl, cores, per_step, pool=pool)
+            rates.append(r)
+            samples.append(s)
     value = statistics.median(rates)
+    kind = "reference" if impl == "refdyn" else "port"
     print(json.dumps({
         "impl": "reference",
         "metric": f"dFD knot-points/sec ({PAPER.get(args.robot, args.robot)} stand-in {args.robot}, "
                   f"{args.alg}, N={args.n}/GPU)",
         "value": value, "unit": "knots/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
-        "steps": len(rates), "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+        "steps": len(rates), "warmup": args.warmup, "ms_per_step": args.n / value * 1e3,
+        "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic seeded states (SURVEY 8d, seed 1)",
         "config": {"workload": f"{args.robot} {args.alg} f64, N={args.n} knots per GPU "
-                               f"(CPU: bounded sample of {sample} knots per step)",
+                               f"(CPU: bounded sample of ~{int(statistics.median(samples))} knots per step, "
+                               "rate extrapolated linearly)",
                    "robot": args.robot, "algorithm": args.alg, "knots_per_gpu": args.n},
-        "cpu_baseline": {"value": value, "unit": "knots/s", "cores": cores, "kind": "port",
-                         "sample": f"{sample} knots per step over {cores} processes", "cpu": cpu_model()},
+        "cpu_baseline": {"value": value, "unit": "knots/s", "cores": cores, "kind": kind,
+                         "impl": "rbdgen.refdyn from baseline/_ref" if kind == "reference" else "oracle port",
+                         "sample": f"~{int(statistics.median(samples))} knots per step over {cores} processes",
+                         "cpu": cpu_model()},
         "e2e": {"value": value, "unit": "knots/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def _relaunch_distributed(gpus):
+    """`bench.py --gpus N` outside torchrun: re-exec under torch.distributed.run."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -489,13 +719,15 @@ def main():
     ap.add_argument("--alg", default="gradFD")
     ap.add_argument("--dtype", default="f64", choices=("f64", "f32"))
     ap.add_argument("--n", type=int, default=1 << 20)
-    ap.add_argument("--cpu-sample", type=int, default=65536,
-                    help="knots per CPU-baseline sample (~10-20 s of work on a 16-core host)")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="wall seconds of CPU-baseline work (sample sized from a one-process calibration)")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        _relaunch_distributed(args.gpus)
     if args.impl == "reference":
         run_reference(args)
     else:

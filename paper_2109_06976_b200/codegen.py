@@ -1816,8 +1816,9 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
                     tag = f"P{pi}{X}"
                     K = f"Knot_{alg}_{dt}_{tag}"
                     try:
+                        po = tn.get("part_over") or {}
                         text, fl, L = _knot_struct(model, alg, dt, K, trees=tuple(trees), zero_fill=zf and pi == 0,
-                                                   fext=fx)
+                                                   fext=fx, over=po.get(pi, po.get(str(pi))))
                         if (L["minb"] * L["bk"] < 32 * int(tn.get("min_warps", 4)) and alg in ("gradID", "gradFD")
                                 and tn.get("split")):
                             raise GenerationError("thread-per-knot occupancy too low; split the program")
