@@ -599,7 +599,7 @@ class _Program:
     def store(self, slot, idx, e):
         self.em.store(int(slot[1]), idx, e)
 
-    def run(self, trees=None, zero_fill=True, cols=None, fext=False, lowmem=False):
+    def run(self, trees=None, zero_fill=True, cols=None, fext=False, lowmem=False, full_window=False):
         """Emit the whole one-knot program.  Every op carries a task tag:
         'in' / 'xf' (input loads, joint transforms: re-materialised by each
         consumer), then per root tree t: rnea0.t, ia.t, minv.t.j, fd.t,
@@ -611,13 +611,16 @@ class _Program:
         dofs = sorted(i for t in part for i in self.trees[t])
         if not dofs or dofs != list(range(dofs[0], dofs[-1] + 1)):
             raise GenerationError(f"part {trees}: its trees must cover a contiguous dof range")
-        em.lo, em.np = dofs[0], len(dofs)
+        # full_window: the whole robot's input row and every joint transform
+        # (re-materialised on demand), so programs of different parts share
+        # one staged row and one sin/cos table (warp-specialised variants)
+        em.lo, em.np = (0, n) if full_window else (dofs[0], len(dofs))
         em.fext = bool(fext)
         em.task = "in"
         self.load_inputs(input_names(alg, fext))
         em.task = "xf"
         for i in range(n):
-            if any(i in self.trees[t] for t in part):
+            if full_window or any(i in self.trees[t] for t in part):
                 self.emit_xform(i)
         stored = set()
         for t, tree in enumerate(self.trees):
@@ -758,6 +761,11 @@ TUNING_DEFAULT = {
     "fs_warps": 8,       # fs: warps per CTA of the fine-grained schedule
     "fs_variants": 4,    # fs: column variants of a gradient program (CTA rows)
     "fs_max_n": 0,       # fs: batch size up to which the fine-grained kernel runs (with "fs" in maps)
+    "ws_variants": 0,    # ws: CTA-row variants of the program (wsched.variant_programs; 0/1: one)
+    "wc_cluster": 1,     # wc: CTAs per thread-block cluster sharing one 32-knot group (DSMEM arena)
+    "wc_warps": 8,       # wc: warps per CTA
+    "wc_variants": 0,    # wc: CTA-row variants
+    "wc_max_n": 0,       # wc: batch size up to which the wc kernel runs (with "wc" in maps)
 }
 TUNED = {}
 # measured on B200 (N = 2^20): chain7 gradFD fp64 is compute-bound at 6 warps/SM
@@ -801,20 +809,34 @@ def tuning(model=None, alg=None, dtype=None):
     return t
 
 
+_GEN_SOURCES = []
+
+
 def _generator_sources():
+    """sha256 of the generator sources (computed once per process)."""
+    if _GEN_SOURCES:
+        return _GEN_SOURCES[0]
     here = os.path.dirname(os.path.abspath(__file__))
     h = hashlib.sha256()
     for f in ("codegen.py", "wsched.py", "fsched.py", os.path.join("csrc", "rbd_runtime.cuh")):
         with open(os.path.join(here, f), "rb") as fh:
             h.update(fh.read())
-    return h.hexdigest()
+    _GEN_SOURCES.append(h.hexdigest())
+    return _GEN_SOURCES[0]
+
+
+_TUNING_KEYS = {}
 
 
 def tuning_key():
     """Build key: generator sources + tuning knobs (a stale build is never reused)."""
     env = os.environ.get("RBD_TUNING", "")
-    return hashlib.sha256((_generator_sources() + json.dumps(TUNING_DEFAULT, sort_keys=True)
-                           + repr(sorted(TUNED.items())) + env).encode()).hexdigest()[:8]
+    key = _TUNING_KEYS.get(env)
+    if key is None:
+        key = hashlib.sha256((_generator_sources() + json.dumps(TUNING_DEFAULT, sort_keys=True)
+                              + repr(sorted(TUNED.items())) + env).encode()).hexdigest()[:8]
+        _TUNING_KEYS[env] = key
+    return key
 
 
 def knots_per_block(model, alg, dtype):
@@ -829,12 +851,13 @@ def stage_outputs(model, alg, dtype, bk):
     return bk * _odd(ext) * es <= tuning(model, alg, dtype)["stage_kb"] * 1024
 
 
-def generate_knot(model, alg, dtype, trees=None, zero_fill=True, cols=None, fext=False, lowmem=False):
+def generate_knot(model, alg, dtype, trees=None, zero_fill=True, cols=None, fext=False, lowmem=False,
+                  full_window=False):
     """The one-knot program as an op list (`_Emit`).  trees: restrict to
     these root trees (a 'part'; its outputs are the trees' blocks);
     zero_fill: also store the structural zeros outside the blocks emitted."""
     return _Program(model, alg, dtype).run(trees, zero_fill, None if cols is None else frozenset(cols), fext,
-                                           lowmem)
+                                           lowmem, full_window)
 
 
 _FLOPS = {"fma": 2, "mul": 1, "add": 1, "sub": 1, "rcp": 1}
@@ -1290,8 +1313,23 @@ def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None
     return head + lines, sc
 
 
+_MODEL_HASH = {}
+
+
 def model_hash(model):
-    return hashlib.sha256(model.fingerprint().encode()).hexdigest()
+    """sha256 of the model's fingerprint (memoised per model object; the
+    fingerprint text is recomputed and compared only when the cached entry's
+    object has been collected and its id reused)."""
+    ent = _MODEL_HASH.get(id(model))
+    if ent is not None and ent[0]() is model:
+        return ent[1]
+    h = hashlib.sha256(model.fingerprint().encode()).hexdigest()
+    try:
+        import weakref
+        _MODEL_HASH[id(model)] = (weakref.ref(model), h)
+    except TypeError:
+        pass
+    return h
 
 
 SM_SMEM = 228 * 1024      # shared memory per SM (sm_100)
@@ -1518,12 +1556,42 @@ def _multi_knot_struct(model, alg, dt, name, progs, nx, over):
     return "\n".join(src)
 
 
-def _ws_struct(model, alg, dt, warps, name=None, trees=None, zero_fill=True, fext=False, em=None):
+def _ws_struct(model, alg, dt, warps, name=None, trees=None, zero_fill=True, fext=False, em=None, variants=0,
+               cluster=1):
     """Device header of the warp-specialised mapping (see wsched.py).  With
     an `em` holding "imp" ops (split columns), the arena is the per-group
-    slice of the split scratch the prefix kernel filled."""
+    slice of the split scratch the prefix kernel filled.  variants > 1: the
+    program is cut into CTA-row variants (wsched.variant_programs; blockIdx.y
+    picks one), each scheduled on its own; outputs go straight to global.
+    cluster > 1: the tasks are scheduled over cluster x warps warps of a
+    thread-block cluster (one 32-knot group per cluster, CTA rank r runs warps
+    [r W, (r + 1) W)); a task reads a value another CTA produced from that
+    CTA's shared-memory arena (DSMEM, ld.shared::cluster) and phases end with
+    a cluster barrier -- each SM streams only its own warps' code."""
     from . import wsched
-    P = wsched.plan(model, alg, dt, warps, trees, zero_fill, fext, em=em)
+    C = max(1, int(cluster))
+    sw = warps * C  # warps the tasks are scheduled over
+    if variants and variants > 1 and em is None and trees is None:
+        progs = wsched.variant_programs(model, alg, dt, variants, fext)
+    else:
+        progs = None
+    if progs is not None and len(progs) > 1:
+        Ps = [wsched.plan(model, alg, dt, sw, em=e) for e in progs]
+        P = dict(Ps[0])
+        na = max(p["sched"].nslots for p in Ps)
+        row = wsched.LANES * P["es"]
+        P["arena_smem"] = row * (P["sin"] + na) <= wsched.SMEM_BUDGET
+        P["stage"] = False
+    else:
+        P = wsched.plan(model, alg, dt, sw, trees, zero_fill, fext, em=em)
+        Ps = [P]
+        na = P["sched"].nslots
+    if C > 1:
+        P = dict(P)
+        P["stage"] = False
+        if not P["arena_smem"] or wsched.LANES * P["es"] * (P["sin"] + na) > wsched.SMEM_BUDGET:
+            raise GenerationError(f"{model.name} {alg} {dt}: the cluster arena must fit shared memory")
+        P["arena_smem"] = True
     em, sched = P["em"], P["sched"]
     n, nin = P["n"], P["nin"]
     T = "double" if dt == "f64" else "float"
@@ -1536,18 +1604,22 @@ def _ws_struct(model, alg, dt, warps, name=None, trees=None, zero_fill=True, fex
     ext = P["ext"]
     src = [
         f"// GENERATED by paper_2109_06976_b200.codegen -- robot {model.name!r}, {alg} {dt}, warp-specialised",
-        f"// {em.flops} flops per knot; {len(sched.task_ops)} tasks in {len(sched.phases)} phases over {warps} warps;",
-        f"// critical path {sched.critical_path()} of {sched.total()} ops; {sched.nslots} arena slots ({ar_space})",
+    ] + [f"// variant {v}: {len(p['sched'].task_ops)} tasks in {len(p['sched'].phases)} phases over {sw} warps"
+         f"{f' ({C} CTAs)' if C > 1 else ''}; "
+         f"critical path {p['sched'].critical_path()} of {p['sched'].total()} ops; {p['sched'].nslots} arena slots"
+         for v, p in enumerate(Ps)] + [
+        f"// {em.flops} flops per knot (variant 0); arena {ar_space}",
         "#pragma once",
         '#include "rbd_runtime.cuh"',
         f"struct {name or f'Knot_{alg}_{dt}'} {{",
         f"  typedef {T} T;",
-        "  static constexpr int MAP = 1;  // warp-specialised: CTA = 32 knots x W warps",
-        f"  static constexpr int W = {warps}, NDOF = {n}, NIN = {nin}, NSC = {P['nsc']};",
+        ("  static constexpr int MAP = 1;  // warp-specialised: CTA = 32 knots x W warps" if C == 1 else
+         "  static constexpr int MAP = 3;  // warp-specialised over a cluster: C CTAs x W warps on 32 knots"),
+        f"  static constexpr int W = {warps}, NDOF = {n}, NIN = {nin}, NSC = {P['nsc']}, NVAR = {len(Ps)}, C = {C};",
         f"  static constexpr int LO = {em.lo}, NP = {em.np};  // input dof window [LO, LO + NP)",
     ] + _input_consts(em.in_layout) + [
         f"  static constexpr int E0 = {ext[0]}, E1 = {ext[1]}, E2 = {ext[2]};",
-        f"  static constexpr int SIN = {P['sin']}, NA = {sched.nslots}, SOUT = {P['sout']};",
+        f"  static constexpr int SIN = {P['sin']}, NA = {na}, SOUT = {P['sout']};",
         f"  static constexpr bool STAGE = {'true' if P['stage'] else 'false'}, "
         f"ARENA_SMEM = {'true' if P['arena_smem'] else 'false'};",
         f"  static constexpr bool ARENA_GROUP = {'true' if P.get('imports') else 'false'};"
@@ -1567,28 +1639,51 @@ def _ws_struct(model, alg, dt, warps, name=None, trees=None, zero_fill=True, fex
             k += 1
     src.append("    (void)s_in; (void)warp; (void)lane;")
     src.append("  }")
-    src.append("  __device__ __forceinline__ static void run_group(int warp, unsigned a_in, arena_t a_ar, "
-               "out_t a0, out_t a1, out_t a2, unsigned valid) {")
+    if C == 1:
+        src.append("  __device__ __forceinline__ static void run_group(int var, int warp, unsigned a_in, arena_t a_ar, "
+                   "out_t a0, out_t a1, out_t a2, unsigned valid) {")
+    else:
+        src.append("  __device__ __forceinline__ static void run_group(int var, int warp, unsigned a_in, arena_t a_ar, "
+                   "const unsigned* a_rem, out_t a0, out_t a1, out_t a2, unsigned valid) {")
+    rem_ops = "".join(f', "r"(a_rem[{r}])' for r in range(C)) if C > 1 else ""
+    sync = "__syncthreads();" if C == 1 else "rbd_cluster_sync();"
     tn = tuning(model, alg, dt)
     ctab = ConstTable(f"rbd_c_{name or f'Knot_{alg}_{dt}'}", dt)
-    for p, phase in enumerate(sched.phases):
-        src.append(f"    // phase {p}")
-        src.append("    switch (warp) {")
-        for w, tasks in enumerate(phase):
-            if not tasks:
-                continue
-            body = wsched.ptx_block(sched, tasks, dt, em.in_total, em.in_total, ar_space, out_space,
-                                    tn["reload_dist"], ctab)
-            src.append(f"    case {w}:  // {', '.join(tasks)}")
-            src.append('      asm volatile("{\\n\\t"')
-            for ln in body:
-                src.append(f'        "{ln}\\n\\t"')
-            src.append(f'        "}}" :: "r"(a_in), {ac}(a_ar), {oc}(a0), {oc}(a1), {oc}(a2), "r"(valid) : "memory");')
-            src.append("      break;")
+    multi = len(Ps) > 1
+    if multi:
+        src.append("    switch (var) {")
+    for v, Pv in enumerate(Ps):
+        sv, emv = Pv["sched"], Pv["em"]
+        if multi:
+            src.append(f"    case {v}: {{")
+        cta_of = None
+        if C > 1:  # value -> CTA rank of the warp producing it
+            wof = {t: w for ph in sv.phases for w, ts in enumerate(ph) for t in ts}
+            cta_of = {r: wof[t] // warps for r, t in sv.export.items()}
+        for p, phase in enumerate(sv.phases):
+            src.append(f"    // variant {v} phase {p}")
+            src.append("    switch (warp) {")
+            for w, tasks in enumerate(phase):
+                if not tasks:
+                    continue
+                body = wsched.ptx_block(sv, tasks, dt, emv.in_total, emv.in_total, ar_space, out_space,
+                                        tn["reload_dist"], ctab, cta_of=cta_of, my_cta=w // warps)
+                src.append(f"    case {w}:  // {', '.join(tasks)}")
+                src.append('      asm volatile("{\\n\\t"')
+                for ln in body:
+                    src.append(f'        "{ln}\\n\\t"')
+                src.append(f'        "}}" :: "r"(a_in), {ac}(a_ar), {oc}(a0), {oc}(a1), {oc}(a2), "r"(valid)'
+                           f'{rem_ops} : "memory");')
+                src.append("      break;")
+            src.append("    default: break;")
+            src.append("    }")
+            src.append(f"    {sync}")
+        if multi:
+            src.append("    } break;")
+    if multi:
         src.append("    default: break;")
         src.append("    }")
-        src.append("    __syncthreads();")
-    src.append("    (void)a_in; (void)a_ar; (void)a0; (void)a1; (void)a2; (void)valid;")
+    src.append("    (void)var; (void)a_in; (void)a_ar; (void)a0; (void)a1; (void)a2; (void)valid;")
     src += ["  }", "};", ""]
     decl = ctab.declaration()
     src = src[:5] + decl + src[5:]  # after the #include
@@ -1791,13 +1886,17 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
                 X = "X" if fx else ""
                 tags = []
                 for mp in maps:
-                    tag = {"ws": "W", "fs": "F"}.get(mp, "T") + X
+                    tag = {"ws": "W", "fs": "F", "wc": "C"}.get(mp, "T") + X
                     K = f"Knot_{alg}_{dt}_{tag}"
-                    if mp == "fs":
+                    if mp == "wc":
+                        text, fl, L = _ws_struct(model, alg, dt, int(tn["wc_warps"]), K, fext=fx,
+                                                 variants=int(tn["wc_variants"]), cluster=int(tn["wc_cluster"]))
+                    elif mp == "fs":
                         text, fl, L = _fs_struct(model, alg, dt, int(tn["fs_warps"]), int(tn["fs_variants"]), K,
                                                  fext=fx)
                     elif mp == "ws":
-                        text, fl, L = _ws_struct(model, alg, dt, int(tn["warps"]), K, fext=fx)
+                        text, fl, L = _ws_struct(model, alg, dt, int(tn["warps"]), K, fext=fx,
+                                                 variants=int(tn.get("ws_variants", 0)))
                     else:
                         text, fl, L = _knot_struct(model, alg, dt, K, fext=fx)
                     if not fx:
@@ -1862,6 +1961,9 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
                 if "fs" in maps:
                     # small batches: the fine-grained schedule (lowest latency)
                     pick = f"N <= {int(tn['fs_max_n'])} ? rbd__launch_{alg}_{dt}_F{X}{args} : ({pick})"
+                if "wc" in maps:
+                    # small batches: one knot group's tasks over a cluster / several CTA rows
+                    pick = f"N <= {int(tn['wc_max_n'])} ? rbd__launch_{alg}_{dt}_C{X}{args} : ({pick})"
                 dispatch += [
                     f'extern "C" int rbd__launch_{alg}_{dt}{"_fext" if fx else ""}(const void* q, const void* qd, '
                     "const void* u, const void* fx,",

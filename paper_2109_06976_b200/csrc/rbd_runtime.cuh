@@ -271,8 +271,8 @@ rbd_ws_kernel(const typename K::T* __restrict__ q, const typename K::T* __restri
       a_ar = (unsigned)__cvta_generic_to_shared(s_ar + lane);
     else if constexpr (K::ARENA_GROUP)  // split columns: the prefix kernel's exports of this group
       a_ar = (unsigned long long)(garena + (size_t)g * K::NA * 32 + lane);
-    else
-      a_ar = (unsigned long long)(garena + (size_t)blockIdx.x * K::NA * 32 + lane);
+    else  // one arena per resident CTA (grid row y of NVAR variant rows)
+      a_ar = (unsigned long long)(garena + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * K::NA * 32 + lane);
     typename K::out_t a0, a1, a2;
     const int kk = lane < nk ? lane : 0;
     if constexpr (K::STAGE) {
@@ -284,7 +284,7 @@ rbd_ws_kernel(const typename K::T* __restrict__ q, const typename K::T* __restri
       a1 = (unsigned long long)(K::E1 ? o1 + (base + kk) * K::E1 : o0);
       a2 = (unsigned long long)(K::E2 ? o2 + (base + kk) * K::E2 : o0);
     }
-    K::run_group(warp, a_in, a_ar, a0, a1, a2, lane < nk ? 1u : 0u);  // ends with a barrier
+    K::run_group(blockIdx.y, warp, a_in, a_ar, a0, a1, a2, lane < nk ? 1u : 0u);  // ends with a barrier
     if constexpr (K::STAGE) {
       {
         T* dst = o0 + base * K::E0;
@@ -407,9 +407,86 @@ rbd_fs_kernel(const typename K::T* __restrict__ q, const typename K::T* __restri
   }
 }
 
+// ---------------------------------------------------------------------------
+// warp-specialised kernel over a thread-block cluster (MAP 3): one cluster of
+// C CTAs x W warps per 32-knot group (lane = knot); CTA rank r runs the tasks
+// the schedule put on warps [r W, (r + 1) W).  Every CTA stages the group's
+// inputs and sin/cos itself; a value produced on another CTA is read from
+// that CTA's shared-memory arena (DSMEM, ld.shared::cluster at the address
+// mapa gives), and every phase ends with a cluster barrier (release/acquire),
+// so an SM streams only its own warps' code.  Persistent over groups.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void rbd_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <class K>
+__global__ void __launch_bounds__(K::W * 32, 1)
+rbd_wc_kernel(const typename K::T* __restrict__ q, const typename K::T* __restrict__ qd,
+              const typename K::T* __restrict__ u, const typename K::T* __restrict__ fx,
+              typename K::T* __restrict__ o0, typename K::T* __restrict__ o1,
+              typename K::T* __restrict__ o2, long long N) {
+  typedef typename K::T T;
+  constexpr int NT = K::W * 32, L = RBD_WS_LANES;
+  extern __shared__ __align__(16) unsigned char rbd_smem[];
+  T* s_in = reinterpret_cast<T*>(rbd_smem);  // [SIN][33]
+  T* s_ar = s_in + K::SIN * L;                // [NA][33]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  unsigned rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const unsigned a_in = (unsigned)__cvta_generic_to_shared(s_in + lane);
+  const unsigned a_ar = (unsigned)__cvta_generic_to_shared(s_ar + lane);
+  unsigned a_rem[K::C];
+#pragma unroll
+  for (int r = 0; r < K::C; ++r) asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a_rem[r]) : "r"(a_ar), "r"(r));
+  rbd_cluster_sync();  // every CTA of the cluster is running before any DSMEM access
+  const long long groups = (N + 31) / 32;
+  const long long ncl = gridDim.x / K::C;
+  for (long long g = blockIdx.x / K::C; g < groups; g += ncl) {
+    const long long base = g * 32;
+    const int nk = (N - base) < 32 ? (int)(N - base) : 32;
+    constexpr int WMAX = 6 * K::NP;
+    constexpr int PMAX = (32 * WMAX + NT - 1) / NT;
+    T v[K::NIN][PMAX];
+#pragma unroll
+    for (int a = 0; a < K::NIN; ++a) {
+      const T* src = (a == 0 ? q : (a == 1 ? qd : (a == 2 ? u : fx))) + base * K::ins(a) + K::ing(a);
+#pragma unroll
+      for (int r = 0; r < (32 * K::inw(a) + NT - 1) / NT; ++r) {
+        const int idx = tid + r * NT;
+        const int k = idx / K::inw(a), j = idx - k * K::inw(a);
+        v[a][r] = (idx < nk * K::inw(a)) ? __ldg(src + k * K::ins(a) + j) : T(0);
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < K::NIN; ++a) {
+#pragma unroll
+      for (int r = 0; r < (32 * K::inw(a) + NT - 1) / NT; ++r) {
+        const int idx = tid + r * NT;
+        if (idx < 32 * K::inw(a)) {
+          const int k = idx / K::inw(a), j = idx - k * K::inw(a);
+          s_in[(K::inr(a) + j) * L + k] = v[a][r];
+        }
+      }
+    }
+    __syncthreads();
+    K::prologue(s_in, warp, lane);
+    __syncthreads();
+    const int kk = lane < nk ? lane : 0;
+    const unsigned long long a0 = (unsigned long long)(o0 + (base + kk) * K::E0);
+    const unsigned long long a1 = (unsigned long long)(K::E1 ? o1 + (base + kk) * K::E1 : o0);
+    const unsigned long long a2 = (unsigned long long)(K::E2 ? o2 + (base + kk) * K::E2 : o0);
+    // phases end with a cluster barrier; the last one also retires every
+    // remote read of this group's arenas before the next group overwrites them
+    K::run_group(blockIdx.y, (int)rank * K::W + warp, a_in, a_ar, a_rem, a0, a1, a2, lane < nk ? 1u : 0u);
+  }
+}
+
 template <class K>
 constexpr size_t rbd_smem_bytes() {
-  if constexpr (K::MAP == 2)
+  if constexpr (K::MAP == 3)
+    return sizeof(typename K::T) * (size_t)RBD_WS_LANES * (K::SIN + K::NA);
+  else if constexpr (K::MAP == 2)
     return sizeof(typename K::T) * (size_t)RBD_WS_LANES * (K::SIN + K::NA + (K::STAGE ? K::SOUT : 0));
   else if constexpr (K::MAP == 1)
     return sizeof(typename K::T) * (size_t)RBD_WS_LANES *
@@ -461,13 +538,38 @@ static int rbd_launch_kernel(const void* q, const void* qd, const void* u, const
     cudaError_t e = cudaSuccess;
     // the large-shared-memory opt-in is per device
     if (smem > 48 * 1024) {
-      if constexpr (K::MAP == 2)
+      if constexpr (K::MAP == 3)
+        e = cudaFuncSetAttribute(rbd_wc_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      else if constexpr (K::MAP == 2)
         e = cudaFuncSetAttribute(rbd_fs_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       else if constexpr (K::MAP == 1)
         e = cudaFuncSetAttribute(rbd_ws_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       else
         e = cudaFuncSetAttribute(rbd_batch_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return (int)e;
+    }
+    if constexpr (K::MAP == 3) {
+      if (K::C > 8) {
+        e = cudaFuncSetAttribute(rbd_wc_kernel<K>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return (int)e;
+      }
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = K::C;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(K::C, K::NVAR);
+      cfg.blockDim = dim3(K::W * 32);
+      cfg.dynamicSmemBytes = smem;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      e = cudaOccupancyMaxActiveClusters(&ncl, rbd_wc_kernel<K>, &cfg);
+      if (e != cudaSuccess) return (int)e;
+      // clusters per variant row
+      c.grid = (ncl > 0 ? ncl : 1) / K::NVAR;
+      if (c.grid < 1) c.grid = 1;
     }
     if constexpr (K::MAP == 2) {
       int per_sm = 0, sms = 0;
@@ -482,9 +584,11 @@ static int rbd_launch_kernel(const void* q, const void* qd, const void* u, const
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rbd_ws_kernel<K>, K::W * 32, smem);
       if (e != cudaSuccess) return (int)e;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      const int grid = (per_sm > 0 ? per_sm : 1) * sms;
+      // CTAs per variant row: the grid has NVAR rows of them
+      int grid = ((per_sm > 0 ? per_sm : 1) * sms) / K::NVAR;
+      if (grid < 1) grid = 1;
       if (!K::ARENA_SMEM && !K::ARENA_GROUP) {
-        e = cudaMalloc(&c.arena, sizeof(T) * (size_t)grid * K::NA * 32);
+        e = cudaMalloc(&c.arena, sizeof(T) * (size_t)grid * K::NVAR * K::NA * 32);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.last, cudaEventDisableTiming);
         if (e != cudaSuccess) return (int)e;
       }
@@ -492,7 +596,25 @@ static int rbd_launch_kernel(const void* q, const void* qd, const void* u, const
     }
     c.ready = true;
   }
-  if constexpr (K::MAP == 2) {
+  if constexpr (K::MAP == 3) {
+    guard.unlock();
+    const long long groups = (N + 31) / 32;
+    const long long ncl = groups < c.grid ? groups : c.grid;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = K::C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)(ncl * K::C), K::NVAR);
+    cfg.blockDim = dim3(K::W * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = (cudaStream_t)stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return (int)cudaLaunchKernelEx(&cfg, rbd_wc_kernel<K>, (const T*)q, (const T*)qd, (const T*)u, (const T*)fx,
+                                   (T*)o0, (T*)o1, (T*)o2, (long long)N);
+  } else if constexpr (K::MAP == 2) {
     guard.unlock();
     const long long groups = (N + 31) / 32;
     const long long grid = groups < c.grid ? groups : c.grid;
@@ -514,7 +636,7 @@ static int rbd_launch_kernel(const void* q, const void* qd, const void* u, const
       cudaError_t e = cudaStreamWaitEvent(st, c.last, 0);
       if (e != cudaSuccess) return (int)e;
     }
-    rbd_ws_kernel<K><<<(unsigned)grid, K::W * 32, smem, st>>>(
+    rbd_ws_kernel<K><<<dim3((unsigned)grid, K::NVAR), K::W * 32, smem, st>>>(
         (const T*)q, (const T*)qd, (const T*)u, (const T*)fx, (T*)o0, (T*)o1, (T*)o2, (long long)N,
         K::ARENA_GROUP ? (T*)xs : (T*)c.arena);
     cudaError_t e = cudaGetLastError();

@@ -161,7 +161,9 @@ def _run(model, alg, args, dtype=None, device=None, f_ext=None, devices=None):
         else:
             xs_check = xs
         for x in xs_check:
-            if not np.all(np.isfinite(x)):
+            # one reduction pass; the elementwise test only if the sum is not
+            # finite (a non-finite entry, or an overflow of finite ones)
+            if not np.isfinite(np.add.reduce(x, axis=None)) and not np.all(np.isfinite(x)):
                 raise ValueError("state vector contains non-finite entries")
         outs = [_host_empty((N, e), ndt) for _, e in codegen.outputs(alg, n)]
         runtime.run_host(lib, alg, dt, xs, outs, N, device=device, f_ext=fx, devices=devices)

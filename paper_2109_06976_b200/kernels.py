@@ -114,6 +114,7 @@ def compile_library(model, force=False, jobs=None, algorithms=codegen.ALGORITHMS
         "flops_per_knot": {f"{a}_{d}": v for (a, d), v in flops.items()},
         "ptxas": _parse_ptxas(log),
         "nvcc_flags": NVCC_FLAGS,
+        "tuning_env": os.environ.get("RBD_TUNING", ""),  # non-empty: an experiment build (tools/variants.sh)
     }
     with open(os.path.join(tmp, "meta.json"), "w") as fh:
         json.dump(meta, fh, indent=1)
@@ -170,11 +171,20 @@ def _bind(lib):
                                    + [ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)])
     for a in codegen.ALGORITHMS:
         for d in codegen.DTYPES:
-            fn = getattr(lib, f"rbd_{a}_{d}")
+            try:
+                fn = getattr(lib, f"rbd_{a}_{d}")
+            except AttributeError:
+                if os.environ.get("RBD_PARTIAL_BUILD") == "1":  # experiment builds of a few entries
+                    continue
+                raise
             fn.argtypes = [_vp] * 6 + [ctypes.c_int64, _vp]
+            fn.restype = ctypes.c_int
             if a in codegen.FEXT_ALGORITHMS:
                 getattr(lib, f"rbd_{a}_{d}_fext").argtypes = [_vp] * 7 + [ctypes.c_int64, _vp]
+                getattr(lib, f"rbd_{a}_{d}_fext").restype = ctypes.c_int
     for s in ABI_SYMBOLS:
+        if not hasattr(lib, s) and os.environ.get("RBD_PARTIAL_BUILD") == "1":
+            continue
         getattr(lib, s).restype = ctypes.c_int
     return lib
 

@@ -151,12 +151,15 @@ class Schedule:
         return sum(self.cost.values())
 
 
-def ptx_block(sched, tasks, dtype, scratch_base, nin_slots, arena_space, out_space, reload_dist=0, ctab=None):
+def ptx_block(sched, tasks, dtype, scratch_base, nin_slots, arena_space, out_space, reload_dist=0, ctab=None,
+              cta_of=None, my_cta=0):
     """PTX for one warp's tasks in one phase.
 
     Operands: %0 = this lane's input-staging address (shared, u32),
     %1 = this lane's arena address (shared u32 or global u64),
-    %2..%4 = this lane's out0..2 address, %5 = knot valid flag.
+    %2..%4 = this lane's out0..2 address, %5 = knot valid flag, and over a
+    cluster %6 + r = this lane's arena address in CTA rank r (shared::cluster,
+    from mapa): a value produced on CTA cta_of[reg] != my_cta is read there.
     Shared [slot][lane] rows are LANES elements apart; a global arena is
     [slot][32 lanes]."""
     em = sched.em
@@ -206,7 +209,10 @@ def ptx_block(sched, tasks, dtype, scratch_base, nin_slots, arena_space, out_spa
         elif tag in REMAT:
             emit(dop)
         elif r in sched.slot:
-            lines.append(f"ld.{arena_space}.{t} {R}{r}, [%1+{sched.slot[r] * arena_stride}];")
+            if cta_of is not None and cta_of.get(r, my_cta) != my_cta:
+                lines.append(f"ld.shared::cluster.{t} {R}{r}, [%{6 + cta_of[r]}+{sched.slot[r] * arena_stride}];")
+            else:
+                lines.append(f"ld.{arena_space}.{t} {R}{r}, [%1+{sched.slot[r] * arena_stride}];")
         else:
             raise cg.GenerationError(f"register {r} used before its definition in task order")
         have[r] = step[0]
@@ -268,6 +274,39 @@ def ptx_block(sched, tasks, dtype, scratch_base, nin_slots, arena_space, out_spa
     if out_space == "global":
         head += [".reg .pred %%p;", "setp.ne.u32 %%p, %5, 0;"]
     return head + lines
+
+
+def variant_programs(model, alg, dtype, k, fext=False):
+    """Split one knot's program over CTA rows ("variants", blockIdx.y) so a
+    small batch spreads over more SMs: one variant per root tree (independent
+    sub-programs), and a tree's gradient columns cut into contiguous groups,
+    about k groups over the whole robot in proportion to tree size; each
+    variant re-computes its tree's prefix (RNEA, Minv, FD) itself.  Every
+    variant reads the whole staged input row (full window) so all CTA rows
+    share one staging layout and sin/cos table.  Entries no variant stores
+    (cross-tree structural zeros) are stored as 0 by the variants, round
+    robin.  Returns the list of op lists (`_Emit`)."""
+    n = model.n_dof
+    trees = [model.subtree(r) for r in model.roots()]
+    grad = alg in ("gradID", "gradFD")
+    progs = []
+    for t, tree in enumerate(trees):
+        groups = [None]
+        if grad:
+            g = max(1, min(len(tree), int(round(k * len(tree) / n))))
+            groups = [tree[i * len(tree) // g:(i + 1) * len(tree) // g] for i in range(g)]
+        for cols in groups:
+            progs.append(cg.generate_knot(model, alg, dtype, trees=(t,), zero_fill=False, cols=cols, fext=fext,
+                                          full_window=True))
+    if alg in ("Minv", "gradID", "gradFD"):
+        stored = {(op[1], op[2]) for em in progs for op in em.ops if op[0] == "st"}
+        outs = (0,) if alg == "Minv" else (0, 1)
+        zeros = [(o, idx) for o in outs for idx in range(n * n) if (o, idx) not in stored]
+        for z, (o, idx) in enumerate(zeros):
+            em = progs[z % len(progs)]
+            em.ops.append(("st", o, idx, 0.0))
+            em.tasks.append("zeros")
+    return progs
 
 
 def plan(model, alg, dtype, warps, trees=None, zero_fill=True, fext=False, em=None):

@@ -13,7 +13,7 @@ import re
 
 import numpy as np
 
-_MEM = re.compile(r"^(@%p )?(ld|st)\.(shared|global)\.(f64|f32) (.*)$")
+_MEM = re.compile(r"^(@%p )?(ld|st)\.(shared::cluster|shared|global)\.(f64|f32) (.*)$")
 _ADDR = re.compile(r"\[%(\d+)\+(\d+)\]")
 _CONST = re.compile(r"^ld\.const\.f64 (\S+), \[(\w+)\+(\d+)\]$")
 

@@ -49,8 +49,8 @@ def run_thread(model, alg, dt, x, stage, budget=None, park=False, fext=False):
     return [np.array([o.get(i, np.nan) for i in range(e)]) for o, (_, e) in zip(outs, codegen.outputs(alg, n))]
 
 
-def run_ws(model, alg, dt, x, warps, arena_space="shared", out_space="shared", fext=False):
-    P = wsched.plan(model, alg, dt, warps, fext=fext)
+def run_ws(model, alg, dt, x, warps, arena_space="shared", out_space="shared", fext=False, em=None, outs=None):
+    P = wsched.plan(model, alg, dt, warps, fext=fext, em=em)
     S = P["sched"]
     n = P["n"]
     nin = P["em"].in_total // n
@@ -61,7 +61,7 @@ def run_ws(model, alg, dt, x, warps, arena_space="shared", out_space="shared", f
         row[nin * n + 2 * k] = math.sin(x[slot])
         row[nin * n + 2 * k + 1] = math.cos(x[slot])
     arena = {}
-    outs = [dict() for _ in range(3)]
+    outs = [dict() for _ in range(3)] if outs is None else outs
     astride = L * es if arena_space == "shared" else 32 * es
     ostride = L * es if out_space == "shared" else es
     ctab = codegen.ConstTable("K", dt)
@@ -99,6 +99,73 @@ def test_device_ptx_matches_reference(name, mapping):
                 ref = g[f"{alg}.{nm}"][k:k + 1]
                 assert np.all(np.isfinite(o)), (name, alg, nm, "unwritten output")
                 assert rel_err(o[None], ref) < 1e-12, (name, alg, nm)
+
+
+@pytest.mark.parametrize("name,k", [("chain7", 4), ("quad12", 4), ("tree7", 3), ("mixed5", 3), ("humanoid30", 8)])
+def test_ws_variants_compose_to_the_whole(name, k):
+    """CTA-row variants (wsched.variant_programs): each variant runs on its
+    own arena; together they write every output element exactly once and
+    match the reference (cross-tree zeros included)."""
+    g = golden(name)
+    m = models.load(name)
+    n = m.n_dof
+    for alg in codegen.ALGORITHMS:
+        progs = wsched.variant_programs(m, alg, "f64", k)
+        if alg in ("gradID", "gradFD"):
+            assert len(progs) >= min(k, n) or len(progs) >= len(m.roots())
+        stores = [(op[1], op[2]) for em in progs for op in em.ops if op[0] == "st"]
+        assert len(stores) == len(set(stores)), (name, alg, "an element is written by two variants")
+        x = _inputs(g, alg, 3, n)
+        outs = [dict() for _ in range(3)]
+        for em in progs:
+            run_ws(m, alg, "f64", x, 5, arena_space="shared", out_space="global", em=em, outs=outs)
+        for (nm, e), o in zip(codegen.outputs(alg, n), outs):
+            got = np.array([o.get(i, np.nan) for i in range(e)])
+            assert np.all(np.isfinite(got)), (name, alg, nm, "unwritten output")
+            assert rel_err(got[None], g[f"{alg}.{nm}"][3:4]) < 1e-12, (name, alg, nm)
+
+
+@pytest.mark.parametrize("name,C", [("chain7", 4), ("quad12", 2), ("mixed5", 3), ("humanoid30", 4)])
+def test_ws_cluster_arena(name, C):
+    """Cluster mapping: tasks over C CTAs x W warps; each value lives in the
+    arena of the CTA whose warp produced it, a consumer on another CTA reads
+    it with ld.shared::cluster through that CTA's operand (%6 + rank)."""
+    g = golden(name)
+    m = models.load(name)
+    n = m.n_dof
+    W = 4
+    L = wsched.LANES
+    for alg in codegen.ALGORITHMS:
+        P = wsched.plan(m, alg, "f64", W * C)
+        S, em = P["sched"], P["em"]
+        x = _inputs(g, alg, 1, n)
+        nin = em.in_total // n
+        row = {i: float(v) for i, v in enumerate(x)}
+        for k, slot in enumerate(_sincos_slots(em)):
+            row[nin * n + 2 * k] = math.sin(x[slot])
+            row[nin * n + 2 * k + 1] = math.cos(x[slot])
+        wof = {t: w for ph in S.phases for w, ts in enumerate(ph) for t in ts}
+        cta_of = {r: wof[t] // W for r, t in S.export.items()}
+        arenas = [dict() for _ in range(C)]
+        outs = [dict() for _ in range(3)]
+        ctab = codegen.ConstTable("K", "f64")
+        remote = 0
+        for phase in S.phases:
+            for w, tasks in enumerate(phase):
+                if not tasks:
+                    continue
+                lines = wsched.ptx_block(S, tasks, "f64", nin * n, nin * n, "shared", "global", 0, ctab,
+                                         cta_of=cta_of, my_cta=w // W)
+                remote += sum("shared::cluster" in ln for ln in lines)
+                ptxsim.run_block(lines, [row, arenas[w // W]] + outs + [None] + arenas,
+                                 [L * 8, L * 8, 8, 8, 8, None] + [L * 8] * C,
+                                 consts={"K": sorted(ctab.index, key=ctab.index.get)})
+        if alg in ("gradFD", "gradID", "Minv"):
+            assert remote > 0, (name, alg, "no value crossed CTAs")
+        for (nm, e), o in zip(codegen.outputs(alg, n), outs):
+            got = np.array([o.get(i, np.nan) for i in range(e)])
+            assert np.all(np.isfinite(got)), (name, alg, nm, "unwritten output")
+            assert rel_err(got[None], g[f"{alg}.{nm}"][1:2]) < 1e-12, (name, alg, nm)
 
 
 def test_ws_schedule_properties():
