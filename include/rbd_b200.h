@@ -171,6 +171,16 @@ int rbd_session_device(const rbd_session* s, int32_t* device);
 int rbd_euler_step(int dtype, const void* q, const void* qd, const void* qdd, void* q_next,
                    void* qd_next, int64_t N, double dt, void* stream);
 
+/* Fused rollout: B trajectories x H semi-implicit Euler steps of FD or gradFD
+ * in ONE launch (a CTA carries a 32-trajectory group through the whole
+ * horizon).  Time-major device arrays: q, qd [H+1][B][n] with step 0 set by
+ * the caller (steps 1..H are written), tau and qdd [H][B][n], and for gradFD
+ * dq, dqd [H][B][n*n] (NULL for FD).  Per step k: qdd_k = FD(q_k, qd_k, tau_k)
+ * (refdyn.py:172; gradFD also writes fd_grad, refdyn.py:242), then
+ * qd_{k+1} = qd_k + dt qdd_k, q_{k+1} = q_k + dt qd_{k+1}. */
+int rbd_rollout(int alg, int dtype, void* q, void* qd, const void* tau, void* qdd, void* dq, void* dqd,
+                int64_t B, int32_t H, double dt, void* stream);
+
 /* Benchmark helper (not in the reference interface): calls rbd_run_host
  * `reps` times back to back and stores the mean host wall time per call in
  * *seconds (steady clock) -- the end-to-end latency a C/C++ caller sees,

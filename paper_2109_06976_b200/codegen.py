@@ -1189,7 +1189,7 @@ def row_homes(em, scratch_base):
     return homes
 
 
-def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None, plan=None):
+def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None, plan=None, tslot=None):
     """Device backend: the op list as PTX for one inline-asm block.
 
     Operand %0 is the 32-bit shared address of the knot's input row (inputs,
@@ -1202,6 +1202,12 @@ def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None
     stream together; reload_dist > 0 re-loads smem-resident values near their
     uses instead of keeping them live.  With a SpillPlan the row also holds
     the values the plan parks: loads and stores follow the plan exactly.
+    tslot: {import register: TMEM slot} -- split-column imports homed in
+    tensor memory (operand %6 = this thread's TMEM address: lane quadrant of
+    its warp, column base): the block starts by copying them scratch -> TMEM
+    (tcgen05.st, 32x32b shape: one TMEM lane per thread, an fp64 = 2
+    columns), and their reloads are tcgen05.ld, waited for (tcgen05.wait::ld)
+    right before the first op that reads one of them.
     Returns (lines, sincos input slots).
     """
     t = em.dtype
@@ -1242,15 +1248,55 @@ def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None
 
     sc = []
     narith = 0
+    tslot = tslot or {}
+    tw = 2 if es == 8 else 1  # TMEM columns per value
+    pending = []               # TMEM loads issued, not yet waited for
+    if tslot:
+        if plan is None:
+            raise GenerationError("TMEM-homed imports need a register plan")
+        items = sorted(tslot.items(), key=lambda x: x[1])
+        for g in range(0, len(items), 16):  # 16 scratch loads in flight, then their TMEM stores
+            grp = items[g:g + 16]
+            for a, _ in grp:
+                lines.append(f"ld.global.{t} {R}{a}, [%5+{plan.gslot[a] * 32 * es}];")
+            for a, ts in grp:
+                if es == 8:
+                    lines.append(f"mov.b64 {{%%tl0, %%th0}}, {R}{a};")
+                    lines.append(f"tcgen05.st.sync.aligned.32x32b.x2.b32 [%6+{tw * ts}], {{%%tl0, %%th0}};")
+                else:
+                    lines.append(f"mov.b32 %%tl0, {R}{a};")
+                    lines.append(f"tcgen05.st.sync.aligned.32x32b.x1.b32 [%6+{tw * ts}], {{%%tl0}};")
+        lines.append("tcgen05.wait::st.sync.aligned;")
+
+    def flush_pending():
+        if pending:
+            lines.append("tcgen05.wait::ld.sync.aligned;")
+            for a in pending:
+                if es == 8:
+                    lines.append(f"mov.b64 {R}{a}, {{%%tl{a}, %%th{a}}};")
+                else:
+                    lines.append(f"mov.b32 {R}{a}, %%tl{a};")
+            pending.clear()
+
     for i, op in enumerate(em.ops):
         k = op[0]
         step += 1
         if plan is not None:
             for a in plan.before.get(i, ()):
-                if a in plan.gslot:  # split columns: import from the knot's scratch slot (L2)
+                if a in tslot:  # TMEM-homed import
+                    if a in pending:
+                        continue
+                    if es == 8:
+                        lines.append(f"tcgen05.ld.sync.aligned.32x32b.x2.b32 {{%%tl{a}, %%th{a}}}, [%6+{tw * tslot[a]}];")
+                    else:
+                        lines.append(f"tcgen05.ld.sync.aligned.32x32b.x1.b32 {{%%tl{a}}}, [%6+{tw * tslot[a]}];")
+                    pending.append(a)
+                elif a in plan.gslot:  # split columns: import from the knot's scratch slot (L2)
                     lines.append(f"ld.global.{t} {R}{a}, [%5+{plan.gslot[a] * 32 * es}];")
                 else:
                     lines.append(f"ld.shared.{t} {R}{a}, [%0+{plan.slot[a] * es}];")
+            if pending and any(a in pending for a in op_srcs(op)):
+                flush_pending()
             if k == "sincos":
                 sc.append(op[3])
                 continue
@@ -1308,6 +1354,8 @@ def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None
         if sync_every and narith % sync_every == 0:
             lines.append("bar.sync 1;")
     head = [f".reg .{t} {R}<{nreg}>;"]
+    if tslot:
+        head.append(f".reg .b32 %%tl<{em.nreg}>, %%th<{em.nreg}>;")  # TMEM load staging (32-bit halves)
     if out_space == "global":
         head += [".reg .pred %%p;", "setp.ne.u32 %%p, %4, 0;"]
     return head + lines, sc
@@ -1419,6 +1467,7 @@ def _struct_head(model, alg, dt, L, fl, name=None):
         f"  static constexpr int FLOPS = {fl};",
         "  static constexpr int MAP = 0;  // thread per knot",
         f"  static constexpr int MINB = {L.get('minb', 1)};  // CTAs per SM the row layout is sized for",
+        f"  static constexpr int TCOLS = {L.get('tcols', 0)};  // TMEM columns per CTA (split-column imports)",
     ]
 
 
@@ -1457,9 +1506,35 @@ def _omap_decl(L, name):
     return lines
 
 
-def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=False, em=None, nx=0, over=None):
+def tmem_homes(plan, count, es):
+    """{import register: TMEM slot} for the `count` split-column imports the
+    plan reloads most often, and the TMEM columns a CTA allocates for them
+    (power of two >= 32; an fp64 takes 2 columns of the thread's lane)."""
+    if not count or plan is None or not plan.gslot:
+        return {}, 0
+    hits = {}
+    for lst in plan.before.values():
+        for a in lst:
+            if a in plan.gslot:
+                hits[a] = hits.get(a, 0) + 1
+    top = sorted(hits, key=lambda a: (-hits[a], a))[:int(count)]
+    cols = (2 if es == 8 else 1) * len(top)
+    if cols == 0:
+        return {}, 0
+    alloc = 32
+    while alloc < cols:
+        alloc *= 2
+    if alloc > 512:
+        raise GenerationError(f"{len(top)} TMEM-homed imports need {cols} columns (> 512)")
+    return {a: k for k, a in enumerate(top)}, alloc
+
+
+def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=False, em=None, nx=0, over=None,
+                 tmem=0):
     """Device header: C++ sin/cos prologue + the PTX body in one asm block.
-    nx > 0: the program exports nx values per knot to the split scratch."""
+    nx > 0: the program exports nx values per knot to the split scratch;
+    tmem > 0: that many of the imports it reloads most are homed in tensor
+    memory (tmem_homes) -- the CTA must be 4 warps (one per TMEM lane quadrant)."""
     if em is None:
         em = generate_knot(model, alg, dt, trees, zero_fill, fext=fext)
     L = _layout(model, alg, dt, em, over=over)
@@ -1468,7 +1543,10 @@ def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=Fal
     tn = tuning(model, alg, dt)
     ctab = ConstTable(f"rbd_c_{name or f'Knot_{alg}_{dt}'}", dt)
     plan = L["plan"]
-    body, sc = ptx_body(em, em.in_total, space, tn["sync_every"], tn["reload_dist"], ctab, plan)
+    tslot, L["tcols"] = tmem_homes(plan, tmem, 8 if dt == "f64" else 4)
+    if tslot and L["bk"] != 128:
+        raise GenerationError("TMEM-homed imports need 128-knot CTAs (one warp per TMEM lane quadrant)")
+    body, sc = ptx_body(em, em.in_total, space, tn["sync_every"], tn["reload_dist"], ctab, plan, tslot=tslot)
     ra = (f"// register budget: {plan.reloads} reloads, {plan.stores} parked values, row {L['sin']} slots, "
           f"{L['minb']} CTAs of {L['bk']} per SM" if plan is not None else "// ptxas register allocation")
     src = [
@@ -1480,15 +1558,17 @@ def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=Fal
     ] + ctab.declaration() + _omap_decl(L, name or f"Knot_{alg}_{dt}") \
         + _struct_head(model, alg, dt, L, em.flops, name) + [
         f"  static constexpr int NX = {nx};  // values exported per knot to the split scratch",
-        "  __device__ __forceinline__ static void run_dev(T* my, T* o0, T* o1, T* o2, unsigned valid, T* xb) {",
     ]
     if L.get("park"):
         nm = name or f"Knot_{alg}_{dt}"
-        src.insert(-1, f"  static constexpr int NOUT = {L['nout']};  // output elements this program writes")
-        src.insert(-1, f"  static constexpr bool OFULL = {'true' if L['ofull'] else 'false'};  // ... all of them, in order")
-        src.insert(-1, f"  __device__ __forceinline__ static const short* omap() {{ return rbd_om_{nm}; }}")
-        src.insert(-1, "  __device__ __forceinline__ static const unsigned short* oelem() { return "
+        src.append(f"  static constexpr int NOUT = {L['nout']};  // output elements this program writes")
+        src.append(f"  static constexpr bool OFULL = {'true' if L['ofull'] else 'false'};  // ... all of them, in order")
+        src.append(f"  __device__ __forceinline__ static const short* omap() {{ return rbd_om_{nm}; }}")
+        src.append("  __device__ __forceinline__ static const unsigned short* oelem() { return "
                    + (f"rbd_oe_{nm}" if not L["ofull"] else "nullptr") + "; }")
+    src += ["  __device__ __forceinline__ static void run_dev(T* my, T* o0, T* o1, T* o2, unsigned valid, T* xb,",
+            "                                                 unsigned tm = 0) {",
+            "    (void)tm;"]
     base = em.in_total
     for k, slot in enumerate(sc):
         src.append(f"    {{ T s, c; rbd_sincos(my[{slot}], &s, &c); my[{base + 2 * k}] = s; my[{base + 2 * k + 1}] = c; }}")
@@ -1496,9 +1576,9 @@ def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=Fal
     if L["stage"]:
         src.append("    const unsigned a0 = (unsigned)__cvta_generic_to_shared(o0), "
                    "a1 = (unsigned)__cvta_generic_to_shared(o1), a2 = (unsigned)__cvta_generic_to_shared(o2);")
-        ops = '"r"(a_in), "r"(a0), "r"(a1), "r"(a2), "r"(valid), "l"(xb)'
+        ops = '"r"(a_in), "r"(a0), "r"(a1), "r"(a2), "r"(valid), "l"(xb), "r"(tm)'
     else:
-        ops = '"r"(a_in), "l"(o0), "l"(o1), "l"(o2), "r"(valid), "l"(xb)'
+        ops = '"r"(a_in), "l"(o0), "l"(o1), "l"(o2), "r"(valid), "l"(xb), "r"(tm)'
     src.append('    asm volatile("{\\n\\t"')
     for ln in body:
         src.append(f'      "{ln}\\n\\t"')
@@ -1537,7 +1617,9 @@ def _multi_knot_struct(model, alg, dt, name, progs, nx, over):
     src = head + decls + _struct_head(model, alg, dt, L0, flops, name) + [
         f"  static constexpr int NX = {nx};  // values per knot in the split scratch",
         f"  static constexpr int NPROG = {len(progs)};",
-        "  __device__ __forceinline__ static void run_dev(T* my, T* o0, T* o1, T* o2, unsigned valid, T* xb) {",
+        "  __device__ __forceinline__ static void run_dev(T* my, T* o0, T* o1, T* o2, unsigned valid, T* xb,",
+        "                                                 unsigned tm = 0) {",
+        "    (void)tm;",
         "    run_prog(blockIdx.y, my, o0, o1, o2, valid, xb);",
         "  }",
         "  __device__ __forceinline__ static void run_prog(int prog, T* my, T* o0, T* o1, T* o2, unsigned valid,",
@@ -1794,16 +1876,25 @@ def host_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
     return files
 
 
-def _launch_unit(alg, dt, tag, K, text):
-    """Translation unit of one kernel: its struct + the internal launcher."""
+def _launch_unit(alg, dt, tag, K, text, rollout=False):
+    """Translation unit of one kernel: its struct + the internal launcher
+    (+ the fused-rollout launcher of a whole-robot warp-specialised FD /
+    gradFD program)."""
+    extra = []
+    if rollout:
+        extra = [
+            f'extern "C" int rbd__rollout_{alg}_{dt}(void* q, void* qd, const void* tau, void* o0, void* o1, void* o2,',
+            "                                int64_t B, int32_t H, double dt, void* stream) {",
+            f"  return rbd_launch_rollout<{K}>(q, qd, tau, o0, o1, o2, B, H, dt, stream);",
+            "}",
+        ]
     return "\n".join([
         text.replace("#pragma once\n", ""),
         f'extern "C" int rbd__launch_{alg}_{dt}_{tag}(const void* q, const void* qd, const void* u, const void* fx,',
         "                                void* o0, void* o1, void* o2, int64_t N, void* stream) {",
         f"  return rbd_launch_kernel<{K}>(q, qd, u, fx, o0, o1, o2, N, stream);",
         "}",
-        "",
-    ])
+    ] + extra + [""])
 
 
 def _big_part_unit(model, alg, dt, tag, K, tn, trees, zero_fill, fx):
@@ -1818,6 +1909,9 @@ def _big_part_unit(model, alg, dt, tag, K, tn, trees, zero_fill, fx):
         pre, progs, nx = split_columns(em, by_task=by_task)
         pf = {"park": False, "prefetch_dist": int(tn.get("split_pf_dist", 96)),
               "prefetch_slack": int(tn.get("split_pf_slack", 12)), "ra_budget": int(tn.get("split_budget", 0))}
+        tmem = int(tn.get("split_tmem", 0))  # imports homed in tensor memory (column kernel, 128-knot CTAs)
+        if tmem:
+            pf["bk"] = 128
         try:
             ta, _, _ = _knot_struct(model, alg, dt, K + "A", em=pre, nx=nx)
             # knots per launch pair: large enough that the prefix kernel fills
@@ -1835,7 +1929,7 @@ def _big_part_unit(model, alg, dt, tag, K, tn, trees, zero_fill, fx):
                 tb = _multi_knot_struct(model, alg, dt, K + "B", progs, nx, pf)
             else:
                 # all columns in one program; outputs stored as they are produced
-                tb, _, _ = _knot_struct(model, alg, dt, K + "B", em=progs, nx=nx, over=pf)
+                tb, _, _ = _knot_struct(model, alg, dt, K + "B", em=progs, nx=nx, over=pf, tmem=tmem)
             return "\n".join([
                 ta.replace("#pragma once\n", ""), tb.replace("#pragma once\n", ""),
                 f'extern "C" int rbd__launch_{alg}_{dt}_{tag}(const void* q, const void* qd, const void* u, '
@@ -1875,6 +1969,7 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
     fp = model_hash(model)
     files, flops, table = {}, {}, {}
     dispatch = []
+    rollouts = set()
     sig = "(const void*, const void*, const void*, const void*, void*, void*, void*, int64_t, void*);"
     args = "(q, qd, u, fx, o0, o1, o2, N, stream)"
     for alg in algorithms:
@@ -1902,7 +1997,10 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
                     if not fx:
                         flops[(alg, dt)] = fl
                     table[(alg, dt, fx)] = (L["nin"], L["ext"], 8 if dt == "f64" else 4)
-                    files[f"k_{alg}_{dt}_{tag}.cu"] = _launch_unit(alg, dt, tag, K, text)
+                    ro = (mp == "ws" and not fx and alg in ("FD", "gradFD") and int(tn.get("ws_variants", 0)) <= 1)
+                    files[f"k_{alg}_{dt}_{tag}.cu"] = _launch_unit(alg, dt, tag, K, text, rollout=ro)
+                    if ro:
+                        rollouts.add((alg, dt))
                     tags.append(tag)
                 # large batches of a robot with several root trees: one kernel per
                 # part (a group of trees), each mapped on its own (thread per knot
@@ -1993,6 +2091,21 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
         "",
     ]
     main += dispatch
+    # fused rollouts (rbd_rollout): FD / gradFD over a horizon in one launch
+    for (alg, dt) in sorted(rollouts):
+        main.append(f'extern "C" int rbd__rollout_{alg}_{dt}(void*, void*, const void*, void*, void*, void*, int64_t, '
+                    "int32_t, double, void*);")
+    main += [
+        'extern "C" int rbd_rollout(int alg, int dtype, void* q, void* qd, const void* tau, void* qdd, void* dq,',
+        "                           void* dqd, int64_t B, int32_t H, double dt, void* stream) {",
+    ]
+    for (alg, dt) in sorted(rollouts):
+        a, d = _ALG_ENUM[alg], (1 if dt == "f64" else 0)
+        call = (f"rbd__rollout_FD_{dt}(q, qd, tau, qdd, nullptr, nullptr, B, H, dt, stream)" if alg == "FD" else
+                f"rbd__rollout_gradFD_{dt}(q, qd, tau, dq, dqd, qdd, B, H, dt, stream)")
+        main.append(f"  if (alg == {a} && dtype == {d}) return {call};")
+    main += ["  (void)q; (void)qd; (void)tau; (void)qdd; (void)dq; (void)dqd; (void)B; (void)H; (void)dt; (void)stream;",
+             "  return RBD_EINVAL;", "}"]
     main += [
         "",
         "static int rbd_ndof() { return %d; }" % n,

@@ -140,6 +140,22 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
     }
   }
   __syncthreads();
+  // tensor memory for the imports a split column kernel homes there: one
+  // allocation per CTA (4 warps, warp w -> TMEM lanes [32 w, 32 w + 32)),
+  // released at the end so the SM's other CTAs can allocate
+  unsigned tm = 0;
+  if constexpr (K::TCOLS > 0) {
+    __shared__ unsigned s_tmem;
+    if ((tid >> 5) == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       (unsigned)__cvta_generic_to_shared(&s_tmem)), "n"(K::TCOLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    tm = s_tmem + ((unsigned)(32 * ((tid >> 5) & 3)) << 16);
+  }
   T* my = s_in + tid * K::SIN;  // this knot's inputs + its sin/cos scratch
   // split prefix kernel: this knot's export slots in the scratch ([32-knot chunk][slot][lane])
   T* xb = K::NX ? xs + ((size_t)((base + tid) >> 5) * K::NX * 32 + ((base + tid) & 31)) : nullptr;
@@ -209,7 +225,13 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
     // padding threads of the last CTA are predicated off
     const long long k = base + (tid < nk ? tid : 0);
     K::run_dev(my, o0 + k * K::E0, K::E1 ? o1 + k * K::E1 : nullptr,
-               K::E2 ? o2 + k * K::E2 : nullptr, tid < nk ? 1u : 0u, xb);
+               K::E2 ? o2 + k * K::E2 : nullptr, tid < nk ? 1u : 0u, xb, tm);
+  }
+  if constexpr (K::TCOLS > 0) {
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if ((tid >> 5) == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(K::TCOLS));
   }
 }
 
@@ -405,6 +427,153 @@ rbd_fs_kernel(const typename K::T* __restrict__ q, const typename K::T* __restri
       __syncthreads();
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// fused rollout (warp-specialised program, FD or gradFD): B trajectories x H
+// semi-implicit Euler steps in ONE launch.  A CTA owns a 32-trajectory group
+// for the whole horizon: per step it stages (q_k, qd_k, tau_k), runs the
+// program (outputs of step k to global), then advances the group's states
+// in place -- qd_{k+1} = qd_k + dt qdd_k, q_{k+1} = q_k + dt qd_{k+1} --
+// before the next step.  Time-major arrays: q, qd [H+1][B][n] (step 0 set by
+// the caller), tau / qdd [H][B][n], gradients [H][B][n*n].  States written in
+// the launch are re-read with plain (coherent) loads, not __ldg.
+// ---------------------------------------------------------------------------
+template <class K>
+__global__ void __launch_bounds__(K::W * 32, K::MINB)
+rbd_ws_rollout_kernel(typename K::T* __restrict__ q, typename K::T* __restrict__ qd,
+                      const typename K::T* __restrict__ tau, typename K::T* __restrict__ o0,
+                      typename K::T* __restrict__ o1, typename K::T* __restrict__ o2, long long B, int H,
+                      typename K::T dt, typename K::T* __restrict__ garena) {
+  typedef typename K::T T;
+  constexpr int n = K::NDOF, NT = K::W * 32, L = RBD_WS_LANES;
+  static_assert(K::LO == 0 && K::NP == K::NDOF && K::NIN == 3 && K::NVAR == 1, "rollout: whole-robot program");
+  // qdd is the last output: FD -> out0 [n], gradFD -> out2 [n]
+  constexpr int EQ = K::E2 ? K::E2 : K::E0;
+  static_assert(EQ == n, "rollout: FD / gradFD programs only");
+  extern __shared__ __align__(16) unsigned char rbd_smem[];
+  T* s_in = reinterpret_cast<T*>(rbd_smem);
+  T* s_ar = s_in + K::SIN * L;
+  T* s_out = s_ar + (K::ARENA_SMEM ? K::NA * L : 0);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long groups = (B + 31) / 32;
+  for (long long g = blockIdx.x; g < groups; g += gridDim.x) {
+    const long long base = g * 32;
+    const int nk = (B - base) < 32 ? (int)(B - base) : 32;
+    for (int k = 0; k < H; ++k) {
+      const size_t st = (size_t)k * B * n;
+      const T* src3[3] = {q + st, qd + st, tau + st};
+      for (int a = 0; a < 3; ++a)
+        for (int idx = tid; idx < 32 * n; idx += NT) {
+          const int kn = idx / n, j = idx - kn * n;
+          s_in[(K::inr(a) + j) * L + kn] = kn < nk ? src3[a][(base + kn) * n + j] : T(0);
+        }
+      __syncthreads();
+      K::prologue(s_in, warp, lane);
+      __syncthreads();
+      const unsigned a_in = (unsigned)__cvta_generic_to_shared(s_in + lane);
+      typename K::arena_t a_ar;
+      if constexpr (K::ARENA_SMEM)
+        a_ar = (unsigned)__cvta_generic_to_shared(s_ar + lane);
+      else
+        a_ar = (unsigned long long)(garena + (size_t)blockIdx.x * K::NA * 32 + lane);
+      T* p0 = o0 + (size_t)k * B * K::E0;
+      T* p1 = K::E1 ? o1 + (size_t)k * B * K::E1 : o0;
+      T* p2 = K::E2 ? o2 + (size_t)k * B * K::E2 : o0;
+      typename K::out_t a0, a1, a2;
+      const int kk = lane < nk ? lane : 0;
+      if constexpr (K::STAGE) {
+        a0 = (unsigned)__cvta_generic_to_shared(s_out + lane);
+        a1 = (unsigned)__cvta_generic_to_shared(s_out + K::E0 * L + lane);
+        a2 = (unsigned)__cvta_generic_to_shared(s_out + (K::E0 + K::E1) * L + lane);
+      } else {
+        a0 = (unsigned long long)(p0 + (base + kk) * K::E0);
+        a1 = (unsigned long long)(p1 + (base + kk) * K::E1);
+        a2 = (unsigned long long)(p2 + (base + kk) * K::E2);
+      }
+      K::run_group(0, warp, a_in, a_ar, a0, a1, a2, lane < nk ? 1u : 0u);  // ends with a barrier
+      if constexpr (K::STAGE) {
+        for (int b = 0; b < 3; ++b) {
+          const int E = b == 0 ? K::E0 : (b == 1 ? K::E1 : K::E2);
+          const int off = b == 0 ? 0 : (b == 1 ? K::E0 : K::E0 + K::E1);
+          T* dst = (b == 0 ? p0 : (b == 1 ? p1 : p2)) + base * E;
+          for (int idx = tid; idx < nk * E; idx += NT) {
+            const int kn = idx / E, e = idx - kn * E;
+            __stcs(dst + idx, s_out[(off + e) * L + kn]);
+          }
+        }
+      }
+      __syncthreads();  // this step's qdd (global or staged) is visible to the whole CTA
+      const T* qddk = (K::E2 ? p2 : p0) + base * n;
+      const size_t nx = (size_t)(k + 1) * B * n;
+      for (int idx = tid; idx < nk * n; idx += NT) {
+        const int kn = idx / n, j = idx - kn * n;
+        const T a = K::STAGE ? s_out[((K::E2 ? K::E0 + K::E1 : 0) + j) * L + kn] : qddk[idx];
+        const T v = qd[st + (base + kn) * n + j] + dt * a;
+        qd[nx + (base + kn) * n + j] = v;
+        q[nx + (base + kn) * n + j] = q[st + (base + kn) * n + j] + dt * v;
+      }
+      __syncthreads();  // next step stages the new states
+    }
+  }
+}
+
+template <class K>
+constexpr size_t rbd_smem_bytes();
+static inline bool rbd_capturing(cudaStream_t s);
+
+template <class K>
+static int rbd_launch_rollout(void* q, void* qd, const void* tau, void* o0, void* o1, void* o2, int64_t B, int32_t H,
+                              double dt, void* stream) {
+  typedef typename K::T T;
+  if (B < 0 || H < 0 || !q || !qd || !tau || !o0 || (K::E1 > 0 && !o1) || (K::E2 > 0 && !o2)) return RBD_EINVAL;
+  if (B == 0 || H == 0) return 0;
+  constexpr size_t smem = rbd_smem_bytes<K>();
+  struct cache_t {
+    std::mutex lock;
+    bool ready = false;
+    int grid = 0;
+    void* arena = nullptr;
+    cudaEvent_t last = nullptr;
+    bool used = false;
+  };
+  static cache_t cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cache_t& c = cache[dev & 63];
+  std::lock_guard<std::mutex> guard(c.lock);
+  cudaError_t e = cudaSuccess;
+  if (!c.ready) {
+    if (smem > 48 * 1024) {
+      e = cudaFuncSetAttribute(rbd_ws_rollout_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return (int)e;
+    }
+    int per_sm = 0, sms = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rbd_ws_rollout_kernel<K>, K::W * 32, smem);
+    if (e != cudaSuccess) return (int)e;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    c.grid = (per_sm > 0 ? per_sm : 1) * sms;
+    if (!K::ARENA_SMEM) {
+      e = cudaMalloc(&c.arena, sizeof(T) * (size_t)c.grid * K::NA * 32);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.last, cudaEventDisableTiming);
+      if (e != cudaSuccess) return (int)e;
+    }
+    c.ready = true;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long groups = (B + 31) / 32;
+  const long long grid = groups < c.grid ? groups : c.grid;
+  // a global arena is indexed by CTA: order launches that share it
+  const bool chain = !K::ARENA_SMEM && !rbd_capturing(st);
+  if (chain && c.used && (e = cudaStreamWaitEvent(st, c.last, 0)) != cudaSuccess) return (int)e;
+  rbd_ws_rollout_kernel<K><<<(unsigned)grid, K::W * 32, smem, st>>>(
+      (T*)q, (T*)qd, (const T*)tau, (T*)o0, (T*)o1, (T*)o2, (long long)B, (int)H, (T)dt, (T*)c.arena);
+  e = cudaGetLastError();
+  if (e == cudaSuccess && chain) {
+    e = cudaEventRecord(c.last, st);
+    c.used = true;
+  }
+  return (int)e;
 }
 
 // ---------------------------------------------------------------------------

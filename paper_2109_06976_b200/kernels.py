@@ -118,8 +118,9 @@ def compile_library(model, force=False, jobs=None, algorithms=codegen.ALGORITHMS
     }
     with open(os.path.join(tmp, "meta.json"), "w") as fh:
         json.dump(meta, fh, indent=1)
+    keep_src = os.environ.get("RBD_KEEP_SOURCES") == "1"  # generated .cu kept for inspection only on request
     for f in os.listdir(tmp):
-        if f.endswith(".o"):
+        if f.endswith(".o") or (not keep_src and f.startswith("k_") and f.endswith(".cu")):
             os.remove(os.path.join(tmp, f))
     shutil.rmtree(bdir, ignore_errors=True)
     os.replace(tmp, bdir)
@@ -145,7 +146,7 @@ class RbdInfo(ctypes.Structure):
 ABI_SYMBOLS = (["rbd_get_info", "rbd_alg_extents", "rbd_launch", "rbd_launch_fext", "rbd_session_create",
                 "rbd_session_destroy", "rbd_run_host", "rbd_run_host_fext", "rbd_bench_host",
                 "rbd_run_host_multi", "rbd_run_host_multi_fext", "rbd_session_device",
-                "rbd_euler_step"]
+                "rbd_euler_step", "rbd_rollout"]
                + [f"rbd_{a}_{d}" for a in codegen.ALGORITHMS for d in codegen.DTYPES]
                + [f"rbd_{a}_{d}_fext" for a in codegen.FEXT_ALGORITHMS for d in codegen.DTYPES])
 
@@ -158,6 +159,8 @@ def _bind(lib):
     lib.rbd_launch.argtypes = [ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp]
     lib.rbd_launch_fext.argtypes = [ctypes.c_int, ctypes.c_int] + [_vp] * 7 + [ctypes.c_int64, _vp]
     lib.rbd_euler_step.argtypes = [ctypes.c_int] + [_vp] * 5 + [ctypes.c_int64, ctypes.c_double, _vp]
+    lib.rbd_rollout.argtypes = [ctypes.c_int, ctypes.c_int] + [_vp] * 6 + [ctypes.c_int64, ctypes.c_int32,
+                                                                            ctypes.c_double, _vp]
     lib.rbd_run_host_fext.argtypes = [_vp, ctypes.c_int, ctypes.c_int] + [_vp] * 7 + [ctypes.c_int64]
     lib.rbd_session_create.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(_vp)]
     lib.rbd_session_destroy.argtypes = [_vp]

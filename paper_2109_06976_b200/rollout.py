@@ -4,14 +4,16 @@ optimization", PAPER.md:10).
 
     traj = rollout(model, q0, qd0, tau, dt, grad=True)
 
-B trajectories of H steps advance entirely on the GPU: per step one batched
-dynamics launch over the B knots (FD, or gradFD when the per-knot Jacobians
-are wanted -- it returns qdd too) and one semi-implicit Euler step
-(`rbd_euler_step`: qd' = qd + dt qdd, q' = q + dt qd').  States are kept
-time-major, [H+1][B][n], so every step's knots are contiguous for the
-batched kernels.  No host synchronisation or copy happens inside the loop;
-`Rollout` captures the H-step launch sequence once in a CUDA graph and
-replays it (the launch-bound regime of small B).
+B trajectories of H steps advance entirely on the GPU.  Default (fused):
+ONE launch of `rbd_rollout` -- each CTA carries a 32-trajectory group
+through the whole horizon, running the warp-specialised FD / gradFD program
+and the semi-implicit Euler update (qd' = qd + dt qdd, q' = q + dt qd')
+step after step with no launch in between.  fused=False keeps the per-step
+form: one batched dynamics launch over the B knots (FD, or gradFD when the
+per-knot Jacobians are wanted -- it returns qdd too) and one
+`rbd_euler_step` per step, captured once in a CUDA graph and replayed.
+States are time-major, [H+1][B][n], so every step's knots are contiguous.
+No host synchronisation or copy happens inside the loop.
 
 Semantics per step k (reference functions restated, refdyn.py:172-175 and
 :242-249): qdd_k = FD(q_k, qd_k, tau_k); with grad=True also
@@ -30,7 +32,7 @@ class Rollout:
     `run(q0, qd0, tau)` fills `q`, `qd` ([H+1, B, n]), `qdd` ([H, B, n]) and,
     with grad, `dq`, `dqd` ([H, B, n, n]) in place."""
 
-    def __init__(self, model, B, H, dt, dtype="f64", grad=False, graph=True, device=None):
+    def __init__(self, model, B, H, dt, dtype="f64", grad=False, graph=True, device=None, fused=True):
         import torch
         self.torch = torch
         self.model, self.B, self.H, self.dt, self.dtype, self.grad = model, int(B), int(H), float(dt), dtype, grad
@@ -47,6 +49,7 @@ class Rollout:
         self.dqd = z(H, B, n, n) if grad else None
         self._graph = None
         self._use_graph = graph
+        self.fused = fused
 
     def _steps(self, stream):
         lib, B, dt = self.lib, self.B, self.dtype
@@ -76,6 +79,14 @@ class Rollout:
         self.qd[0].copy_(qd0)
         self.tau.copy_(tau.transpose(0, 1))
         stream = torch.cuda.current_stream(self.device)
+        if self.fused:
+            vp = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None
+            rc = self.lib.rbd_rollout(4 if self.grad else 2, _DT[self.dtype], vp(self.q), vp(self.qd), vp(self.tau),
+                                      vp(self.qdd), vp(self.dq), vp(self.dqd), ctypes.c_int64(self.B),
+                                      ctypes.c_int32(self.H), ctypes.c_double(self.dt),
+                                      ctypes.c_void_p(stream.cuda_stream))
+            runtime.check(rc, "rbd_rollout")
+            return self
         if not self._use_graph:
             self._steps(stream.cuda_stream)
             return self
@@ -101,11 +112,11 @@ class Rollout:
         return tuple(out)
 
 
-def rollout(model, q0, qd0, tau, dt, grad=False, graph=False):
+def rollout(model, q0, qd0, tau, dt, grad=False, graph=False, fused=True):
     """One-shot rollout of B = q0.shape[0] trajectories over H = tau.shape[1]
     steps (CUDA tensors); returns `Rollout.trajectories()`."""
     dtype = "f32" if q0.dtype == __import__("torch").float32 else "f64"
-    r = Rollout(model, q0.shape[0], tau.shape[1], dt, dtype, grad, graph)
+    r = Rollout(model, q0.shape[0], tau.shape[1], dt, dtype, grad, graph, fused=fused)
     return r.run(q0, qd0, tau).trajectories()
 
 

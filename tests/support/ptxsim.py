@@ -37,6 +37,28 @@ def run_block(lines, regions, strides, valid=1, f32=False, consts=None, regs=Non
         ln = raw.replace("%%", "%").strip().rstrip(";")
         if not ln or ln.startswith(".reg") or ln.startswith("setp") or ln.startswith("bar.sync"):
             continue
+        if ln.startswith("tcgen05."):  # tensor memory: one lane (this thread), columns by offset
+            if ".wait::" in ln:
+                continue
+            a = re.search(r"\[%(\d+)\+(\d+)\]", ln)
+            k, off = int(a.group(1)), int(a.group(2))
+            regs_ = re.search(r"\{([^}]*)\}", ln).group(1).split(",")
+            first = regs_[0].strip()
+            if ln.startswith("tcgen05.st"):
+                regions[k][off] = regs[first]
+            else:
+                for r_ in regs_:
+                    regs[r_.strip()] = regions[k][off]
+            continue
+        if ln.startswith("mov.b64 {") or ln.startswith("mov.b32 %tl"):  # split a value into 32-bit halves
+            dst, src = ln.split(" ", 1)[1].rsplit(",", 1)
+            for r_ in dst.strip("{} ").split(","):
+                regs[r_.strip()] = regs[src.strip()]
+            continue
+        if ln.startswith("mov.b64 %") and "{" in ln:  # join halves
+            dst, src = ln.split(" ", 1)[1].split(",", 1)
+            regs[dst.strip()] = regs[src.strip().strip("{}").split(",")[0].strip()]
+            continue
         c = _CONST.match(ln)
         if c:
             regs[c.group(1)] = consts[c.group(2)][int(c.group(3)) // 8]

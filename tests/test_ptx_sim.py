@@ -349,6 +349,21 @@ def test_split_prefix_and_columns(name, trees, alg):
     touts = [dict(o) for o in outs]
     ptxsim.run_block(lines, [crow] + touts + [None, dict(scratch)], [8, 8, 8, 8, 8, 32 * 8],
                      consts={"K": sorted(ctab.index, key=ctab.index.get)})
+    # the same with the most-reloaded imports homed in tensor memory
+    tslot, tcols = codegen.tmem_homes(cplan, 24, 8)
+    assert tslot and tcols >= 2 * len(tslot)
+    ctab = codegen.ConstTable("K", "f64")
+    lines, sc = codegen.ptx_body(cols, cols.in_total, "global", ctab=ctab, plan=cplan, tslot=tslot)
+    assert sum("tcgen05.ld" in ln for ln in lines) > 0
+    mouts = [dict(o) for o in outs]
+    mrow = {i: float(v) for i, v in enumerate(x)}  # a fresh row (the run above recycled input slots)
+    for j, slot in enumerate(sc):
+        mrow[cols.in_total + 2 * j] = math.sin(x[slot])
+        mrow[cols.in_total + 2 * j + 1] = math.cos(x[slot])
+    ptxsim.run_block(lines, [mrow] + mouts + [None, dict(scratch), {}], [8, 8, 8, 8, 8, 32 * 8, 1],
+                     consts={"K": sorted(ctab.index, key=ctab.index.get)})
+    for a, b in zip(mouts, touts):
+        assert a == b
     # one program per gradient column (the product kernel's layout): sin/cos
     # exported too, each program reading only what it uses
     pre2, progs, nx2 = codegen.split_columns(em, by_task=True)

@@ -12,24 +12,27 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("name", ["chain7", "quad12"])
-@pytest.mark.parametrize("graph", [False, True])
-def test_rollout_matches_oracle(name, graph):
+@pytest.mark.parametrize("name,B,H", [("chain7", 37, 6), ("quad12", 5, 6), ("humanoid30", 33, 2)])
+@pytest.mark.parametrize("mode", ["fused", "launches", "graph"])
+def test_rollout_matches_oracle(name, B, H, mode):
+    """fused: one rbd_rollout launch over the horizon (2 trajectory groups,
+    the last ragged, for chain7 / humanoid30; humanoid30's program uses the
+    global arena); launches / graph: per-step launches, direct or replayed."""
     from paper_2109_06976_b200.rollout import Rollout
     m = models.load(name)
     n = m.n_dof
-    B, H, dt = 5, 6, 0.01
+    dt = 0.01
     rng = np.random.default_rng(3)
     q0, qd0 = rng.uniform(-1, 1, (B, n)), rng.uniform(-1, 1, (B, n))
     tau = rng.uniform(-1, 1, (B, H, n))
-    r = Rollout(m, B, H, dt, "f64", grad=True, graph=graph)
+    r = Rollout(m, B, H, dt, "f64", grad=True, graph=(mode == "graph"), fused=(mode == "fused"))
     dev = lambda x: torch.from_numpy(x).cuda()
     for _ in range(2):  # the second call replays the captured graph
         r.run(dev(q0), dev(qd0), dev(tau))
     torch.cuda.synchronize()
     q, qd, qdd, dq, dqd = (x.cpu().numpy() for x in r.trajectories())
-    # oracle, stepped identically
-    for b in range(B):
+    # oracle, stepped identically (a sample of the trajectories for the big robot)
+    for b in (range(B) if n < 20 else (0, B - 1)):
         qb, qdb = q0[b].copy(), qd0[b].copy()
         for k in range(H):
             ref = R.evaluate(m, "gradFD", qb, qdb, tau[b, k])
