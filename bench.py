@@ -472,26 +472,31 @@ def sweep(torch, stream, peaks, args):
     # device-resident rollouts (rollout.py): B trajectories x H steps of gradFD + Euler, graph-replayed
     from paper_2109_06976_b200 import models
     from paper_2109_06976_b200.rollout import Rollout
-    for robot, B, H in (("chain7", 128, 64), ("chain7", 4096, 64), ("humanoid30", 128, 32)):
+    for robot, B, H in (("chain7", 128, 64), ("chain7", 4096, 64), ("quad12", 128, 64), ("humanoid30", 128, 32)):
         m = models.load(robot)
         n = m.n_dof
-        r = Rollout(m, B, H, 0.01, "f64", grad=True, graph=True)
         rng = np.random.default_rng(1)
         q0 = torch.from_numpy(rng.uniform(-1, 1, (B, n))).cuda()
         tau = torch.from_numpy(rng.uniform(-1, 1, (B, H, n))).cuda()
-        for _ in range(3):
-            r.run(q0, q0, tau)
-        st = torch.cuda.current_stream()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
-        for _ in range(10):
-            r.run(q0, q0, tau)
-        e1.record(st)
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / 10
-        out.append({"robot": robot, "paper_robot": PAPER.get(robot), "alg": "rollout(gradFD+Euler)", "dtype": "f64",
-                    "N": B * H, "trajectories": B, "horizon": H, "kernel_us": ms * 1e3,
-                    "kernel_knots_per_s": B * H / (ms * 1e-3), "graph": True})
+        for fused in (True, False):
+            # fused: one rbd_rollout launch over the horizon; else 2 launches per
+            # step (gradFD + Euler) replayed from a CUDA graph
+            r = Rollout(m, B, H, 0.01, "f64", grad=True, graph=True, fused=fused)
+            for _ in range(3):
+                r.run(q0, q0, tau)
+            st = torch.cuda.current_stream()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(10):
+                r.run(q0, q0, tau)
+            e1.record(st)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / 10
+            out.append({"robot": robot, "paper_robot": PAPER.get(robot), "alg": "rollout(gradFD+Euler)",
+                        "dtype": "f64", "N": B * H, "trajectories": B, "horizon": H, "kernel_us": ms * 1e3,
+                        "kernel_knots_per_s": B * H / (ms * 1e-3),
+                        "mode": "fused (1 launch)" if fused else f"graph ({2 * H} launches)"})
+            del r
     # BASELINE configs[4]: large batches (iiwa, HyQ, Atlas up to 1M knots)
     big = {"chain7": (65536, 262144, 1048576), "quad12": (65536, 1048576), "humanoid30": (65536, 262144, 1048576)}
     for robot, Ns in big.items():

@@ -774,10 +774,9 @@ TUNED[("chain7", "gradFD", "f64")] = {"park": False, "bk": 32}
 # 32-knot CTAs: finer-grained CTA turnover (staging / write-back barriers),
 # measured 1.35 -> 1.22 ms (fp64) and 0.64 -> 0.60 ms (fp32) at N = 2^20
 TUNED[("chain7", "gradFD", "f32")] = {"bk": 32}
-for _a in ALGORITHMS:
-    for _d in DTYPES:
-        # small batches: the fine-grained warp-specialised schedule (fsched.py)
-        TUNED.setdefault(("chain7", _a, _d), {}).update({"maps": ["thread", "ws", "fs"], "fs_max_n": 1024})
+# the fine-grained schedule ("fs", fsched.py) measured slower than the task
+# schedule at every small N for chain7 (gradFD fp64 N=128: 10.7 vs 9.9 us;
+# ID: 3.4 vs 2.9 us; profiles/small_n_r2.md), so no robot compiles it by default
 for _a in ALGORITHMS:
     for _d in DTYPES:
         # measured on B200: with outputs parked in the row, quad12's
@@ -785,6 +784,12 @@ for _a in ALGORITHMS:
         # (3.4x the warp-specialised one); humanoid30's one-knot program
         # (~600 live values) does not fit a thread
         TUNED[("quad12", _a, _d)] = {"warps": 16, "minb": 1, "ws_max_n": 4096}  # thread ahead from 8192
+        if _a in ("gradID", "gradFD"):
+            # small batches: CTA-row variants (per leg x column group) spread a
+            # 32-knot group over 8 SMs; measured gradFD N=128 fp64 6.2 -> 4.4 us,
+            # fp32 5.1 -> 3.3 us (and slower than one CTA from N=1024)
+            TUNED[("quad12", _a, _d)].update({"maps": ["thread", "ws", "wc"], "wc_warps": 16, "wc_variants": 8,
+                                              "wc_max_n": 256})
         # humanoid30: small batches on the warp-specialised kernel; large ones
         # per root tree (torso tree, two legs)
         TUNED[("humanoid30", _a, _d)] = {"maps": ["ws"], "warps": 16, "minb": 1, "parts": [[0], [1], [2]],
@@ -797,6 +802,12 @@ for _a in ALGORITHMS:
                                          "split_chunk": 32768 if _d == "f64" else 24576,
                                          # column-kernel register budget (fp64: 80 + 12 prefetch beat 107 + 12)
                                          "split_budget": 80 if _d == "f64" else 0}
+        if _a in ("gradID", "gradFD"):
+            # small batches: 10 CTA-row variants (torso column groups + legs) of
+            # 8 warps; measured gradFD N=256 fp64 95 -> 41 us, fp32 63 -> 36 us,
+            # N=1024 fp64 98 -> 83 us (slower than one CTA per group from 4096)
+            TUNED[("humanoid30", _a, _d)].update({"maps": ["ws", "wc"], "wc_warps": 8, "wc_variants": 10,
+                                                  "wc_max_n": 1024})
 
 
 def tuning(model=None, alg=None, dtype=None):

@@ -159,8 +159,9 @@ def _bind(lib):
     lib.rbd_launch.argtypes = [ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp]
     lib.rbd_launch_fext.argtypes = [ctypes.c_int, ctypes.c_int] + [_vp] * 7 + [ctypes.c_int64, _vp]
     lib.rbd_euler_step.argtypes = [ctypes.c_int] + [_vp] * 5 + [ctypes.c_int64, ctypes.c_double, _vp]
-    lib.rbd_rollout.argtypes = [ctypes.c_int, ctypes.c_int] + [_vp] * 6 + [ctypes.c_int64, ctypes.c_int32,
-                                                                            ctypes.c_double, _vp]
+    if hasattr(lib, "rbd_rollout") or os.environ.get("RBD_PARTIAL_BUILD") != "1":
+        lib.rbd_rollout.argtypes = [ctypes.c_int, ctypes.c_int] + [_vp] * 6 + [ctypes.c_int64, ctypes.c_int32,
+                                                                                ctypes.c_double, _vp]
     lib.rbd_run_host_fext.argtypes = [_vp, ctypes.c_int, ctypes.c_int] + [_vp] * 7 + [ctypes.c_int64]
     lib.rbd_session_create.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(_vp)]
     lib.rbd_session_destroy.argtypes = [_vp]
