@@ -766,6 +766,7 @@ TUNING_DEFAULT = {
     "wc_warps": 8,       # wc: warps per CTA
     "wc_variants": 0,    # wc: CTA-row variants
     "wc_max_n": 0,       # wc: batch size up to which the wc kernel runs (with "wc" in maps)
+    "rollout_fused": True,  # rollout.Rollout default: one rbd_rollout launch (else per-step launches)
 }
 TUNED = {}
 # measured on B200 (N = 2^20): chain7 gradFD fp64 is compute-bound at 6 warps/SM
@@ -808,6 +809,11 @@ for _a in ALGORITHMS:
             # N=1024 fp64 98 -> 83 us (slower than one CTA per group from 4096)
             TUNED[("humanoid30", _a, _d)].update({"maps": ["ws", "wc"], "wc_warps": 8, "wc_variants": 10,
                                                   "wc_max_n": 1024})
+        # the fused rollout runs the one-CTA warp-specialised program (no
+        # CTA-row variants: a step's Euler update needs all of a group's
+        # outputs); measured B=128 x 32 steps gradFD fp64: fused 2.80 ms vs
+        # per-step launches of the variant kernel 1.16 ms
+        TUNED[("humanoid30", _a, _d)]["rollout_fused"] = False
 
 
 def tuning(model=None, alg=None, dtype=None):

@@ -1116,38 +1116,52 @@ static int rbd_run_host_impl(rbd_session* s, int alg, int dtype, const void* q, 
   for (int a = 0; a < e->n_inputs; ++a) in_bytes += (size_t)(N * iext[a]) * es;
   for (int b = 0; b < 3; ++b) out_bytes += (size_t)(N * ext[b]) * es;
   if (in_bytes + out_bytes + 8 * 256 <= RBD_ZC_BYTES) {
-    // zero-copy: device pointers of pinned caller buffers, else the pinned stage
+    // small batch: the kernel reads its inputs straight from pinned host
+    // memory (the caller's buffers when page-locked, else the pinned stage);
+    // outputs go to device memory and come back with ONE copy -- a kernel
+    // writing over PCIe pays per store, and the small-batch kernels' stores
+    // are not all coalesced (CTA-row variants store straight from registers)
     const void* din[4] = {nullptr, nullptr, nullptr, nullptr};
     void* dout[3] = {nullptr, nullptr, nullptr};
-    bool direct = true;
-    for (int a = 0; a < e->n_inputs && direct; ++a) direct = (din[a] = rbd_mapped(hin[a])) != nullptr;
-    for (int b = 0; b < 3 && direct; ++b)
-      if (ext[b]) direct = (dout[b] = (void*)rbd_mapped(hout[b])) != nullptr;
+    bool direct_in = true, direct_out = true;
+    for (int a = 0; a < e->n_inputs && direct_in; ++a) direct_in = (din[a] = rbd_mapped(hin[a])) != nullptr;
     unsigned char* hp = s->hstage;
-    if (!direct) {
+    if (!direct_in) {
       for (int a = 0; a < e->n_inputs; ++a) {
         const size_t bytes = (size_t)(N * iext[a]) * es;
         memcpy(hp, hin[a], bytes);
         din[a] = rbd_mapped(hp);
         hp += rbd_align256(bytes);
       }
-      for (int b = 0; b < 3; ++b) {
-        if (!ext[b]) continue;
-        dout[b] = (void*)rbd_mapped(hp);
-        hp += rbd_align256((size_t)(N * ext[b]) * es);
-      }
+    }
+    // outputs contiguous in the device slot, copied back in one transfer to
+    // the pinned stage (then to the caller) or straight into a pinned caller
+    // buffer per output
+    unsigned char* dp = s->dbuf[0];
+    for (int b = 0; b < 3; ++b) {
+      if (!ext[b]) continue;
+      dout[b] = dp;
+      dp += rbd_align256((size_t)(N * ext[b]) * es);
+      direct_out = direct_out && rbd_mapped(hout[b]) != nullptr;
     }
     cudaStream_t st = s->stream[0];
     rc = e->fn(din[0], din[1], din[2], din[3], dout[0], dout[1], dout[2], N, (void*)st);
+    unsigned char* ho = s->hstage + rbd_align256(in_bytes) + 4 * 256;  // after the staged inputs
+    if (rc == 0) {
+      if (direct_out) {
+        for (int b = 0; b < 3 && rc == 0; ++b)
+          if (ext[b])
+            rc = (int)cudaMemcpyAsync(hout[b], dout[b], (size_t)(N * ext[b]) * es, cudaMemcpyDeviceToHost, st);
+      } else {
+        rc = (int)cudaMemcpyAsync(ho, s->dbuf[0], (size_t)(dp - s->dbuf[0]), cudaMemcpyDeviceToHost, st);
+      }
+    }
     if (rc == 0) rc = (int)cudaStreamSynchronize(st);
-    if (rc == 0 && !direct) {
-      hp = s->hstage;
-      for (int a = 0; a < e->n_inputs; ++a) hp += rbd_align256((size_t)(N * iext[a]) * es);
+    if (rc == 0 && !direct_out) {
       for (int b = 0; b < 3; ++b) {
         if (!ext[b]) continue;
         const size_t bytes = (size_t)(N * ext[b]) * es;
-        memcpy(hout[b], hp, bytes);
-        hp += rbd_align256(bytes);
+        memcpy(hout[b], ho + ((unsigned char*)dout[b] - s->dbuf[0]), bytes);
       }
     }
     cudaSetDevice(prev);

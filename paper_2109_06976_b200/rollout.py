@@ -32,7 +32,7 @@ class Rollout:
     `run(q0, qd0, tau)` fills `q`, `qd` ([H+1, B, n]), `qdd` ([H, B, n]) and,
     with grad, `dq`, `dqd` ([H, B, n, n]) in place."""
 
-    def __init__(self, model, B, H, dt, dtype="f64", grad=False, graph=True, device=None, fused=True):
+    def __init__(self, model, B, H, dt, dtype="f64", grad=False, graph=True, device=None, fused=None):
         import torch
         self.torch = torch
         self.model, self.B, self.H, self.dt, self.dtype, self.grad = model, int(B), int(H), float(dt), dtype, grad
@@ -49,6 +49,9 @@ class Rollout:
         self.dqd = z(H, B, n, n) if grad else None
         self._graph = None
         self._use_graph = graph
+        if fused is None:  # per-robot measured choice (codegen TUNED "rollout_fused")
+            from . import codegen
+            fused = bool(codegen.tuning(model, "gradFD" if grad else "FD", dtype).get("rollout_fused", True))
         self.fused = fused
 
     def _steps(self, stream):
@@ -112,7 +115,7 @@ class Rollout:
         return tuple(out)
 
 
-def rollout(model, q0, qd0, tau, dt, grad=False, graph=False, fused=True):
+def rollout(model, q0, qd0, tau, dt, grad=False, graph=False, fused=None):
     """One-shot rollout of B = q0.shape[0] trajectories over H = tau.shape[1]
     steps (CUDA tensors); returns `Rollout.trajectories()`."""
     dtype = "f32" if q0.dtype == __import__("torch").float32 else "f64"
