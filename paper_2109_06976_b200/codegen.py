@@ -1538,12 +1538,20 @@ def tmem_homes(plan, count, es):
     cols = (2 if es == 8 else 1) * len(top)
     if cols == 0:
         return {}, 0
+    return {a: k for k, a in enumerate(top)}, cols
+
+
+def tmem_alloc(cols_per_thread, bk):
+    """TMEM columns a CTA of bk threads allocates when each thread needs
+    cols_per_thread columns of its lane: warps w and w + 4 share lane
+    quadrant w % 4 and split the columns (power of two >= 32, <= 512)."""
+    per = bk // 128
     alloc = 32
-    while alloc < cols:
+    while alloc < cols_per_thread * per:
         alloc *= 2
     if alloc > 512:
-        raise GenerationError(f"{len(top)} TMEM-homed imports need {cols} columns (> 512)")
-    return {a: k for k, a in enumerate(top)}, alloc
+        raise GenerationError(f"{cols_per_thread} TMEM columns x {per} warps per quadrant exceed 512")
+    return alloc
 
 
 def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=False, em=None, nx=0, over=None,
@@ -1560,9 +1568,10 @@ def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=Fal
     tn = tuning(model, alg, dt)
     ctab = ConstTable(f"rbd_c_{name or f'Knot_{alg}_{dt}'}", dt)
     plan = L["plan"]
-    tslot, L["tcols"] = tmem_homes(plan, tmem, 8 if dt == "f64" else 4)
-    if tslot and L["bk"] != 128:
-        raise GenerationError("TMEM-homed imports need 128-knot CTAs (one warp per TMEM lane quadrant)")
+    tslot, tc = tmem_homes(plan, tmem, 8 if dt == "f64" else 4)
+    if tslot and L["bk"] % 128:
+        raise GenerationError("TMEM-homed imports need CTAs of 4k warps (warps spread over the TMEM lane quadrants)")
+    L["tcols"] = tmem_alloc(tc, L["bk"]) if tslot else 0
     body, sc = ptx_body(em, em.in_total, space, tn["sync_every"], tn["reload_dist"], ctab, plan, tslot=tslot)
     ra = (f"// register budget: {plan.reloads} reloads, {plan.stores} parked values, row {L['sin']} slots, "
           f"{L['minb']} CTAs of {L['bk']} per SM" if plan is not None else "// ptxas register allocation")
@@ -1928,7 +1937,7 @@ def _big_part_unit(model, alg, dt, tag, K, tn, trees, zero_fill, fx):
               "prefetch_slack": int(tn.get("split_pf_slack", 12)), "ra_budget": int(tn.get("split_budget", 0))}
         tmem = int(tn.get("split_tmem", 0))  # imports homed in tensor memory (column kernel, 128-knot CTAs)
         if tmem:
-            pf["bk"] = 128
+            pf["bk"] = int(tn.get("split_bk", 128))  # 4k warps per CTA over the TMEM lane quadrants
         try:
             ta, _, _ = _knot_struct(model, alg, dt, K + "A", em=pre, nx=nx)
             # knots per launch pair: large enough that the prefix kernel fills

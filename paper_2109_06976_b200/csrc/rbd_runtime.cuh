@@ -141,7 +141,7 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
   }
   __syncthreads();
   // tensor memory for the imports a split column kernel homes there: one
-  // allocation per CTA (4 warps, warp w -> TMEM lanes [32 w, 32 w + 32)),
+  // allocation per CTA (4k warps, warp w -> TMEM lanes [32 (w % 4), +32)),
   // released at the end so the SM's other CTAs can allocate
   unsigned tm = 0;
   if constexpr (K::TCOLS > 0) {
@@ -154,7 +154,8 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
-    tm = s_tmem + ((unsigned)(32 * ((tid >> 5) & 3)) << 16);
+    // lane quadrant of the warp; warps w and w + 4 (, w + 8 ...) split the columns
+    tm = s_tmem + ((unsigned)(32 * ((tid >> 5) & 3)) << 16) + (unsigned)((tid >> 7) * (K::TCOLS / (BK / 128)));
   }
   T* my = s_in + tid * K::SIN;  // this knot's inputs + its sin/cos scratch
   // split prefix kernel: this knot's export slots in the scratch ([32-knot chunk][slot][lane])
@@ -231,7 +232,7 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if ((tid >> 5) == 0)
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(K::TCOLS));
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(K::TCOLS));  // warp 0: tm is the allocation base
   }
 }
 

@@ -43,7 +43,10 @@ def _nvcc():
 
 
 def build_dir(model):
-    return os.path.join(BUILD, f"{model.name}-{codegen.model_hash(model)[:16]}-{codegen.tuning_key()}")
+    # RBD_BUILD_KEY: a fixed key for tuning experiments (tools/variants.sh), so
+    # an experiment build stays addressable while the generator keeps changing
+    key = os.environ.get("RBD_BUILD_KEY") or codegen.tuning_key()
+    return os.path.join(BUILD, f"{model.name}-{codegen.model_hash(model)[:16]}-{key}")
 
 
 def library_path(model):

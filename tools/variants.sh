@@ -7,6 +7,7 @@
 mode=$1; robot=$2; alg=$3; dt=$4; shift 4
 while read -r v; do
   [ -z "$v" ] && continue
+  export RBD_BUILD_KEY=x$(printf '%s' "$v" | md5sum | cut -c1-7)
   if [ "$mode" = build ]; then
     RBD_TUNING="$v" python -c "
 import sys; sys.path.insert(0,'.')
