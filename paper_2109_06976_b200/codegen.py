@@ -814,6 +814,12 @@ for _a in ALGORITHMS:
         # outputs); measured B=128 x 32 steps gradFD fp64: fused 2.80 ms vs
         # per-step launches of the variant kernel 1.16 ms
         TUNED[("humanoid30", _a, _d)]["rollout_fused"] = False
+        if _d == "f64":
+            # the 128 most re-read split-column imports homed in tensor memory
+            # and CTA lockstep every 256 ops: gradFD N=2^18 7.46 -> 7.11 ms
+            # (ncu r2d: column kernel long-scoreboard stalls 26.8 -> 11.3 per
+            # issue, DRAM 1.32 -> 0.86 GB per 32768 knots; then fetch-bound)
+            TUNED[("humanoid30", _a, _d)].update({"split_tmem": 128, "sync_every": 256})
 
 
 def tuning(model=None, alg=None, dtype=None):
