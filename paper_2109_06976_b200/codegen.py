@@ -1212,7 +1212,8 @@ def row_homes(em, scratch_base):
     return homes
 
 
-def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None, plan=None, tslot=None):
+def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None, plan=None, tslot=None,
+             trow=False, row_base=0):
     """Device backend: the op list as PTX for one inline-asm block.
 
     Operand %0 is the 32-bit shared address of the knot's input row (inputs,
@@ -1231,6 +1232,12 @@ def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None
     (tcgen05.st, 32x32b shape: one TMEM lane per thread, an fp64 = 2
     columns), and their reloads are tcgen05.ld, waited for (tcgen05.wait::ld)
     right before the first op that reads one of them.
+    trow: the whole row lives in tensor memory (operand %6; row slot s = TMEM
+    columns [2 s, 2 s + 2) for fp64): the block starts by copying the staged
+    inputs and sin/cos (smem row slots [0, row_base)) into their TMEM homes and
+    a CTA barrier (the output staging aliases the input staging); spills are
+    tcgen05.st, reloads tcgen05.ld (a reload of a slot stored since the last
+    tcgen05.wait::st waits for the stores first).
     Returns (lines, sincos input slots).
     """
     t = em.dtype
@@ -1274,6 +1281,41 @@ def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None
     tslot = tslot or {}
     tw = 2 if es == 8 else 1  # TMEM columns per value
     pending = []               # TMEM loads issued, not yet waited for
+    st_pending = set()         # TMEM row slots stored since the last tcgen05.wait::st
+
+    def tst(col, reg):
+        """store register `reg` (value id) to TMEM column `col`"""
+        if es == 8:
+            lines.append(f"mov.b64 {{%%tl{reg}, %%th{reg}}}, {R}{reg};")
+            lines.append(f"tcgen05.st.sync.aligned.32x32b.x2.b32 [%6+{col}], {{%%tl{reg}, %%th{reg}}};")
+        else:
+            lines.append(f"mov.b32 %%tl{reg}, {R}{reg};")
+            lines.append(f"tcgen05.st.sync.aligned.32x32b.x1.b32 [%6+{col}], {{%%tl{reg}}};")
+
+    def tld(col, reg):
+        if es == 8:
+            lines.append(f"tcgen05.ld.sync.aligned.32x32b.x2.b32 {{%%tl{reg}, %%th{reg}}}, [%6+{col}];")
+        else:
+            lines.append(f"tcgen05.ld.sync.aligned.32x32b.x1.b32 {{%%tl{reg}}}, [%6+{col}];")
+
+    if trow:
+        if plan is None:
+            raise GenerationError("a TMEM row needs a register plan")
+        # home slots [0, row_base): staged inputs and the sin/cos the C++
+        # prologue wrote; copied through scratch registers %rt (one per slot)
+        for g in range(0, row_base, 16):
+            grp = range(g, min(g + 16, row_base))
+            for sl in grp:
+                lines.append(f"ld.shared.{t} %%rt{sl}, [%0+{sl * es}];")
+            for sl in grp:
+                if es == 8:
+                    lines.append(f"mov.b64 {{%%rl{sl}, %%rh{sl}}}, %%rt{sl};")
+                    lines.append(f"tcgen05.st.sync.aligned.32x32b.x2.b32 [%6+{tw * sl}], {{%%rl{sl}, %%rh{sl}}};")
+                else:
+                    lines.append(f"mov.b32 %%rl{sl}, %%rt{sl};")
+                    lines.append(f"tcgen05.st.sync.aligned.32x32b.x1.b32 [%6+{tw * sl}], {{%%rl{sl}}};")
+        lines.append("tcgen05.wait::st.sync.aligned;")
+        lines.append("bar.sync 1;")  # every thread's inputs are in TMEM: the staging may now take outputs
     if tslot:
         if plan is None:
             raise GenerationError("TMEM-homed imports need a register plan")
@@ -1316,6 +1358,15 @@ def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None
                     pending.append(a)
                 elif a in plan.gslot:  # split columns: import from the knot's scratch slot (L2)
                     lines.append(f"ld.global.{t} {R}{a}, [%5+{plan.gslot[a] * 32 * es}];")
+                elif trow:
+                    if a in pending:
+                        continue
+                    sl = plan.slot[a]
+                    if sl in st_pending:
+                        lines.append("tcgen05.wait::st.sync.aligned;")
+                        st_pending.clear()
+                    tld(tw * sl, a)
+                    pending.append(a)
                 else:
                     lines.append(f"ld.shared.{t} {R}{a}, [%0+{plan.slot[a] * es}];")
             if pending and any(a in pending for a in op_srcs(op)):
@@ -1372,13 +1423,20 @@ def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None
             raise GenerationError(f"unknown op {k}")
         if plan is not None:
             for v, sl in plan.after.get(i, ()):
-                lines.append(f"st.shared.{t} [%0+{sl * es}], {R}{v};")
+                if trow:
+                    tst(tw * sl, v)
+                    st_pending.add(sl)
+                else:
+                    lines.append(f"st.shared.{t} [%0+{sl * es}], {R}{v};")
         narith += 1
         if sync_every and narith % sync_every == 0:
             lines.append("bar.sync 1;")
     head = [f".reg .{t} {R}<{nreg}>;"]
-    if tslot:
+    if tslot or trow:
         head.append(f".reg .b32 %%tl<{em.nreg}>, %%th<{em.nreg}>;")  # TMEM load staging (32-bit halves)
+    if trow:
+        head.append(f".reg .{t} %%rt<{max(row_base, 1)}>;")
+        head.append(f".reg .b32 %%rl<{max(row_base, 1)}>, %%rh<{max(row_base, 1)}>;")
     if out_space == "global":
         head += [".reg .pred %%p;", "setp.ne.u32 %%p, %4, 0;"]
     return head + lines, sc
@@ -1428,6 +1486,32 @@ def _layout(model, alg, dt, em, device=True, over=None):
     base = em.in_total + 2 * nsc
     sout = _odd(sum(ext))
     plan, minb = None, 1
+    if tn.get("tmem_row") and tn.get("ra") and device:
+        # the knot's row (inputs, sin/cos, spilled values) lives in tensor
+        # memory, one TMEM lane per thread (2 columns per fp64): 4-warp CTAs,
+        # 2 per SM (8 warps, 255 registers), each CTA 256 columns; shared
+        # memory only stages the inputs and then, aliased over them, the
+        # outputs in element order for the coalesced write-back
+        bk = 128
+        tcols_thread = 256
+        budget = (255 - REG_OVERHEAD) // (2 if dt == "f64" else 1)
+        if tn.get("ra_budget"):
+            budget = min(budget, int(tn["ra_budget"]))
+        pf = None
+        if tn.get("prefetch_dist"):
+            pf = (int(tn["prefetch_dist"]), int(tn["prefetch_slack"]))
+            budget -= pf[1]
+        homes = row_homes(em, em.in_total)
+        plan = SpillPlan(em, budget, homes, base, park_outputs=False, prefetch=pf)
+        tw = 2 if es == 8 else 1
+        if plan.nslots * tw > tcols_thread:
+            raise GenerationError(f"{model.name} {alg} {dt}: row of {plan.nslots} slots exceeds a TMEM lane")
+        row = _odd(base)
+        smem = bk * max(row, sout) * es
+        if 2 * (smem + CTA_SMEM_RESERVED) > SM_SMEM:
+            raise GenerationError(f"{model.name} {alg} {dt}: output staging does not fit 2 CTAs per SM")
+        return dict(n=n, ext=ext, nin=nin, nsc=nsc, bk=bk, stage=True, sin=row, sout=sout, plan=plan, minb=2,
+                    park=False, lo=em.lo, np=em.np, in_layout=em.in_layout, trow=True, tcols=tcols_thread)
     if tn.get("ra") and device:
         homes = row_homes(em, em.in_total)
         for warps in range(int(tn["warps_per_sm"]), 1, -1):
@@ -1490,7 +1574,9 @@ def _struct_head(model, alg, dt, L, fl, name=None):
         f"  static constexpr int FLOPS = {fl};",
         "  static constexpr int MAP = 0;  // thread per knot",
         f"  static constexpr int MINB = {L.get('minb', 1)};  // CTAs per SM the row layout is sized for",
-        f"  static constexpr int TCOLS = {L.get('tcols', 0)};  // TMEM columns per CTA (split-column imports)",
+        f"  static constexpr int TCOLS = {L.get('tcols', 0)};  // TMEM columns per CTA (split-column imports / row)",
+        f"  static constexpr bool TROW = {'true' if L.get('trow') else 'false'};  // the row lives in TMEM; "
+        "outputs staged over the input staging",
     ]
 
 
@@ -1574,11 +1660,16 @@ def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=Fal
     tn = tuning(model, alg, dt)
     ctab = ConstTable(f"rbd_c_{name or f'Knot_{alg}_{dt}'}", dt)
     plan = L["plan"]
-    tslot, tc = tmem_homes(plan, tmem, 8 if dt == "f64" else 4)
-    if tslot and L["bk"] % 128:
-        raise GenerationError("TMEM-homed imports need CTAs of 4k warps (warps spread over the TMEM lane quadrants)")
-    L["tcols"] = tmem_alloc(tc, L["bk"]) if tslot else 0
-    body, sc = ptx_body(em, em.in_total, space, tn["sync_every"], tn["reload_dist"], ctab, plan, tslot=tslot)
+    if L.get("trow"):
+        tslot = {}
+    else:
+        tslot, tc = tmem_homes(plan, tmem, 8 if dt == "f64" else 4)
+        if tslot and L["bk"] % 128:
+            raise GenerationError("TMEM-homed imports need CTAs of 4k warps (warps spread over the TMEM lane "
+                                  "quadrants)")
+        L["tcols"] = tmem_alloc(tc, L["bk"]) if tslot else 0
+    body, sc = ptx_body(em, em.in_total, space, tn["sync_every"], tn["reload_dist"], ctab, plan, tslot=tslot,
+                        trow=bool(L.get("trow")), row_base=L["sin"] if L.get("trow") else 0)
     ra = (f"// register budget: {plan.reloads} reloads, {plan.stores} parked values, row {L['sin']} slots, "
           f"{L['minb']} CTAs of {L['bk']} per SM" if plan is not None else "// ptxas register allocation")
     src = [

@@ -100,7 +100,10 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
   constexpr int BK = K::BK, n = K::NDOF;
   extern __shared__ __align__(16) unsigned char rbd_smem[];
   T* s_in = reinterpret_cast<T*>(rbd_smem);  // [BK][SIN], SIN odd -> conflict-free rows
-  T* s_out = s_in + BK * K::SIN;             // [BK][SOUT] when staging
+  // [BK][SOUT] when staging; with the row in TMEM (TROW) the output staging
+  // aliases the input staging (the program copies its inputs to TMEM and
+  // passes a CTA barrier before its first output store)
+  T* s_out = K::TROW ? s_in : s_in + BK * K::SIN;
   const long long base = (long long)blockIdx.x * BK;
   const long long left = N - base;
   const int nk = left < BK ? (int)left : BK;
@@ -164,7 +167,7 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
   if constexpr (K::PARK) {
     // the program parks every output value in its row; write the CTA's
     // contiguous output ranges back coalesced (structural zeros from the map)
-    K::run_dev(my, nullptr, nullptr, nullptr, 1u, xb);
+    K::run_dev(my, nullptr, nullptr, nullptr, 1u, xb, tm);
     __syncthreads();
     if constexpr (rbd_nout<K>() == 0) {
       // nothing parked (a split prefix whose outputs all come from the columns)
@@ -197,7 +200,7 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
     }
   } else if constexpr (K::STAGE) {
     T* o = s_out + tid * K::SOUT;
-    K::run_dev(my, o, o + K::E0, o + K::E0 + K::E1, 1u, xb);
+    K::run_dev(my, o, o + K::E0, o + K::E0 + K::E1, 1u, xb, tm);
     __syncthreads();
     // coalesced write-back, one output array at a time
     {
@@ -661,6 +664,8 @@ constexpr size_t rbd_smem_bytes() {
   else if constexpr (K::MAP == 1)
     return sizeof(typename K::T) * (size_t)RBD_WS_LANES *
            (K::SIN + (K::ARENA_SMEM ? K::NA : 0) + (K::STAGE ? K::SOUT : 0));
+  else if constexpr (K::TROW)  // input staging and output staging aliased
+    return sizeof(typename K::T) * (size_t)K::BK * (K::SIN > K::SOUT ? K::SIN : K::SOUT);
   else
     return sizeof(typename K::T) * (size_t)K::BK * (K::SIN + (K::STAGE ? K::SOUT : 0)) +
            sizeof(short) * (size_t)rbd_nout<K>() * (rbd_ofull<K>() ? 1 : 2);

@@ -22,24 +22,28 @@ def _sincos_slots(em):
     return [op[3] for op in em.ops if op[0] == "sincos"]
 
 
-def run_thread(model, alg, dt, x, stage, budget=None, park=False, fext=False):
+def run_thread(model, alg, dt, x, stage, budget=None, park=False, fext=False, trow=False):
     em = codegen.generate_knot(model, alg, dt, fext=fext)
     n = model.n_dof
     nin = em.in_total // n
     ctab = codegen.ConstTable("K", dt)
     plan = None
+    nsc = len(_sincos_slots(em))
     if budget:
-        nsc = len(_sincos_slots(em))
         plan = codegen.SpillPlan(em, budget, codegen.row_homes(em, nin * n), nin * n + 2 * nsc,
                                  park_outputs=park)
-    lines, sc = codegen.ptx_body(em, nin * n, "shared" if stage else "global", ctab=ctab, plan=plan)
+    lines, sc = codegen.ptx_body(em, nin * n, "shared" if stage else "global", ctab=ctab, plan=plan,
+                                 trow=trow, row_base=nin * n + 2 * nsc)
+    if trow:
+        assert sum("tcgen05.ld" in ln for ln in lines) > 0 and not any("st.shared.f" in ln and "%0+" in ln
+                                                                       for ln in lines)
     es = 8 if dt == "f64" else 4
     row = {i: float(v) for i, v in enumerate(x)}
     for k, slot in enumerate(sc):
         row[nin * n + 2 * k] = math.sin(x[slot])
         row[nin * n + 2 * k + 1] = math.cos(x[slot])
     outs = [dict() for _ in range(3)]
-    ptxsim.run_block(lines, [row] + outs + [None], [es] * 5, f32=(dt == "f32"),
+    ptxsim.run_block(lines, [row] + outs + [None, None, {}], [es] * 5 + [8, 1], f32=(dt == "f32"),
                      consts={"K": sorted(ctab.index, key=ctab.index.get)})
     if park:  # the kernel's write-back: parked row slots, structural zeros
         for (k, idx), sl in plan.outslot.items():
@@ -75,7 +79,7 @@ def run_ws(model, alg, dt, x, warps, arena_space="shared", out_space="shared", f
 
 
 @pytest.mark.parametrize("name", ["pendulum2", "chain7", "tree7", "mixed5", "quad12"])
-@pytest.mark.parametrize("mapping", ["thread", "thread_ra", "thread_park", "ws"])
+@pytest.mark.parametrize("mapping", ["thread", "thread_ra", "thread_park", "thread_trow", "ws"])
 def test_device_ptx_matches_reference(name, mapping):
     g = golden(name)
     m = models.load(name)
@@ -88,6 +92,9 @@ def test_device_ptx_matches_reference(name, mapping):
             elif mapping == "thread_park":
                 # the product layout: outputs parked in the row, written back by map
                 outs = run_thread(m, alg, "f64", x, stage=False, budget=16 if k == 0 else 119, park=True)
+            elif mapping == "thread_trow":
+                # the row in tensor memory (inputs copied in, spills / reloads as tcgen05.st / ld)
+                outs = run_thread(m, alg, "f64", x, stage=True, budget=12 if k == 0 else 40, trow=True)
             elif mapping == "thread_ra":
                 # tight register budgets force heavy parking / slot reuse
                 outs = run_thread(m, alg, "f64", x, stage=(k == 0), budget=12 if k == 0 else 40)
