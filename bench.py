@@ -63,6 +63,7 @@ REF_IR_FLOPS = {  # BASELINE.md §3, counted on the reference's generated IR (FM
     ("humanoid30", "gradID"): 57839, ("humanoid30", "gradFD"): 96220,
 }
 PAPER = {"chain7": "iiwa", "quad12": "HyQ", "humanoid30": "Atlas"}
+HEADLINE_PROFILE = "ncu_summary_r2i.json"  # `ncu --set full` of the current headline kernel (tools/gpu_final.sh)
 N_IN = {"ID": 3, "Minv": 1, "FD": 3, "gradID": 3, "gradFD": 3}
 
 
@@ -592,15 +593,28 @@ def run_ours(args):
     # `ncu --set full` capture (profiles/ncu_summary_r<k>.json)
     import glob
     import re
+    # (keys "<robot>_<alg>_<dt>" = a 2^20-knot launch, or "<robot>_<alg>_<dt>_<N>")
     profs = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_summary_r*.json")),
                    key=lambda f: (int(re.search(r"_r(\d+)", f).group(1)), f))
+    # the capture of the current headline kernel first (round 2: r2i)
+    cur = os.path.join(ROOT, "profiles", HEADLINE_PROFILE)
+    if cur in profs:
+        profs.remove(cur)
+        profs.append(cur)
+    head = f"{robot}_{alg}_{dt}"
     for prof in reversed(profs):
         try:
-            t = json.load(open(prof)).get(f"{robot}_{alg}_{dt}", {}).get("dram_bytes_per_launch")
+            d = json.load(open(prof))
         except Exception:
-            t = None
-        if t:
-            traffic, traffic_src = t * N / (1 << 20), os.path.relpath(prof, ROOT)
+            continue
+        for key, rec in d.items():
+            m = re.fullmatch(re.escape(head) + r"(?:_(\d+))?", key)
+            t = rec.get("dram_bytes_per_launch") if m and isinstance(rec, dict) else None
+            if t:
+                n_prof = int(m.group(1)) if m.group(1) else (1 << 20)
+                traffic, traffic_src = t * N / n_prof, f"{os.path.relpath(prof, ROOT)} [{key}]"
+                break
+        if traffic:
             break
 
     n_gpus = 1 if shared else world

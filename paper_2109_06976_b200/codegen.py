@@ -2249,9 +2249,11 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
                 if (alg, dt, fx) in table:
                     nin, ext, es = table[(alg, dt, fx)]
                     fn = f"rbd__launch_{alg}_{dt}{'_fext' if fx else ''}"
-                    pair.append(f"{{&{fn}, {nin}, {ext[0]}, {ext[1]}, {ext[2]}, {es}}}")
+                    tn = tuning(model, alg, dt)
+                    cmax = int(tn["wc_max_n"]) if "wc" in tn["maps"] else 0
+                    pair.append(f"{{&{fn}, {nin}, {ext[0]}, {ext[1]}, {ext[2]}, {es}, {cmax}}}")
                 else:
-                    pair.append("{nullptr, 0, 0, 0, 0, 0}")
+                    pair.append("{nullptr, 0, 0, 0, 0, 0, 0}")
             row.append("{" + ", ".join(pair) + "}")
         main.append("    {" + ", ".join(row) + "},")
     main += [

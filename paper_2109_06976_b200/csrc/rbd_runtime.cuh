@@ -971,7 +971,10 @@ struct rbd_entry {
   rbd_launch_fn fn;
   int32_t n_inputs;
   int64_t e0, e1, e2;
-  int32_t elem;  // sizeof(T)
+  int32_t elem;           // sizeof(T)
+  int64_t copy_out_max_n;  // batches up to this size run a kernel whose output stores are not
+                           // coalesced (CTA-row variants): the small-batch host path lands its
+                           // outputs in device memory and copies them back once
 };
 #if defined(RBD_MAIN_TU)
 static const rbd_entry* rbd_entry_for(int alg, int dtype, int fext);  // generated main TU
@@ -1140,20 +1143,35 @@ static int rbd_run_host_impl(rbd_session* s, int alg, int dtype, const void* q, 
         hp += rbd_align256(bytes);
       }
     }
-    // outputs contiguous in the device slot, copied back in one transfer to
-    // the pinned stage (then to the caller) or straight into a pinned caller
-    // buffer per output
+    // kernels that stage their outputs write them coalesced straight into
+    // pinned host memory; the others (N <= copy_out_max_n) write device
+    // memory, copied back in one transfer to the pinned stage (then to the
+    // caller) or straight into each pinned caller buffer
+    const bool via_device = N <= e->copy_out_max_n;
     unsigned char* dp = s->dbuf[0];
     for (int b = 0; b < 3; ++b) {
       if (!ext[b]) continue;
+      void* mapped = (void*)rbd_mapped(hout[b]);
+      direct_out = direct_out && mapped != nullptr;
       dout[b] = dp;
       dp += rbd_align256((size_t)(N * ext[b]) * es);
-      direct_out = direct_out && rbd_mapped(hout[b]) != nullptr;
+    }
+    if (!via_device) {  // zero-copy outputs: the caller's pinned buffers, else the pinned stage
+      unsigned char* hq = s->hstage + rbd_align256(in_bytes) + 4 * 256;
+      for (int b = 0; b < 3; ++b) {
+        if (!ext[b]) continue;
+        if (direct_out) {
+          dout[b] = (void*)rbd_mapped(hout[b]);
+        } else {
+          dout[b] = (void*)rbd_mapped(hq);
+          hq += rbd_align256((size_t)(N * ext[b]) * es);
+        }
+      }
     }
     cudaStream_t st = s->stream[0];
     rc = e->fn(din[0], din[1], din[2], din[3], dout[0], dout[1], dout[2], N, (void*)st);
     unsigned char* ho = s->hstage + rbd_align256(in_bytes) + 4 * 256;  // after the staged inputs
-    if (rc == 0) {
+    if (rc == 0 && via_device) {
       if (direct_out) {
         for (int b = 0; b < 3 && rc == 0; ++b)
           if (ext[b])
@@ -1164,10 +1182,12 @@ static int rbd_run_host_impl(rbd_session* s, int alg, int dtype, const void* q, 
     }
     if (rc == 0) rc = (int)cudaStreamSynchronize(st);
     if (rc == 0 && !direct_out) {
+      unsigned char* src = ho;
       for (int b = 0; b < 3; ++b) {
         if (!ext[b]) continue;
         const size_t bytes = (size_t)(N * ext[b]) * es;
-        memcpy(hout[b], ho + ((unsigned char*)dout[b] - s->dbuf[0]), bytes);
+        memcpy(hout[b], src, bytes);
+        src += rbd_align256(bytes);
       }
     }
     cudaSetDevice(prev);
