@@ -1716,7 +1716,7 @@ def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=Fal
     return "\n".join(src), em.flops, L
 
 
-def _multi_knot_struct(model, alg, dt, name, progs, nx, over):
+def _multi_knot_struct(model, alg, dt, name, progs, nx, over, tmem=0):
     """One thread-per-knot kernel holding several one-knot programs (the
     gradient columns of a split program); CTA row blockIdx.y runs program
     blockIdx.y, so every warp of a CTA streams the same (short) code.  All
@@ -1736,23 +1736,31 @@ def _multi_knot_struct(model, alg, dt, name, progs, nx, over):
         '#include "rbd_runtime.cuh"',
     ]
     bodies, decls = [], []
+    tcols = 0
+    if tmem and L0["bk"] % 128:
+        raise GenerationError("TMEM-homed imports need CTAs of 4k warps")
     for k, (p, L) in enumerate(zip(progs, Ls)):
         ctab = ConstTable(f"rbd_c_{name}_{k}", dt)
-        body, sc = ptx_body(p, p.in_total, "global", 0, 0, ctab, L["plan"])
+        # each program homes ITS most re-read imports in tensor memory
+        tslot, tc = tmem_homes(L["plan"], tmem, 8 if dt == "f64" else 4)
+        if tslot:
+            tcols = max(tcols, tmem_alloc(tc, L0["bk"]))
+        body, sc = ptx_body(p, p.in_total, "global", 0, 0, ctab, L["plan"], tslot=tslot)
         if sc:
             raise GenerationError("column programs import their sin/cos")
         decls += ctab.declaration()
         bodies.append((p.tasks[-1], body))
+    L0["tcols"] = tcols
     src = head + decls + _struct_head(model, alg, dt, L0, flops, name) + [
         f"  static constexpr int NX = {nx};  // values per knot in the split scratch",
         f"  static constexpr int NPROG = {len(progs)};",
         "  __device__ __forceinline__ static void run_dev(T* my, T* o0, T* o1, T* o2, unsigned valid, T* xb,",
         "                                                 unsigned tm = 0) {",
-        "    (void)tm;",
-        "    run_prog(blockIdx.y, my, o0, o1, o2, valid, xb);",
+        "    run_prog(blockIdx.y, my, o0, o1, o2, valid, xb, tm);",
         "  }",
         "  __device__ __forceinline__ static void run_prog(int prog, T* my, T* o0, T* o1, T* o2, unsigned valid,",
-        "                                                  T* xb) {",
+        "                                                  T* xb, unsigned tm) {",
+        "    (void)tm;",
         "    const unsigned a_in = (unsigned)__cvta_generic_to_shared(my);",
         "    switch (prog) {",
     ]
@@ -1761,7 +1769,7 @@ def _multi_knot_struct(model, alg, dt, name, progs, nx, over):
         src.append('      asm volatile("{\\n\\t"')
         for ln in body:
             src.append(f'        "{ln}\\n\\t"')
-        src.append('        "}" :: "r"(a_in), "l"(o0), "l"(o1), "l"(o2), "r"(valid), "l"(xb) : "memory");')
+        src.append('        "}" :: "r"(a_in), "l"(o0), "l"(o1), "l"(o2), "r"(valid), "l"(xb), "r"(tm) : "memory");')
         src.append("      break;")
     src += ["    default: break;", "    }", "  }", "};", ""]
     return "\n".join(src)
@@ -2055,7 +2063,7 @@ def _big_part_unit(model, alg, dt, tag, K, tn, trees, zero_fill, fx):
                 # structural zeros (memset) has no work
                 progs = [p for p in progs if any(op[0] != "st" or not isinstance(op[3], float)
                                                  for op, t in zip(p.ops, p.tasks) if t.startswith("grad."))]
-                tb = _multi_knot_struct(model, alg, dt, K + "B", progs, nx, pf)
+                tb = _multi_knot_struct(model, alg, dt, K + "B", progs, nx, pf, tmem=tmem)
             else:
                 # all columns in one program; outputs stored as they are produced
                 tb, _, _ = _knot_struct(model, alg, dt, K + "B", em=progs, nx=nx, over=pf, tmem=tmem)
