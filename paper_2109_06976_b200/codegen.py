@@ -767,6 +767,9 @@ TUNING_DEFAULT = {
     "wc_variants": 0,    # wc: CTA-row variants
     "wc_max_n": 0,       # wc: batch size up to which the wc kernel runs (with "wc" in maps)
     "rollout_fused": True,  # rollout.Rollout default: one rbd_rollout launch (else per-step launches)
+    "wsplit_groups": 6,  # wsplit: column groups of the big tree (CTA-row variants of kernel B)
+    "wsplit_warps": 16,  # wsplit: warps of the prefix kernel A
+    "wsplit_max_n": 0,   # wsplit: batch size up to which the split small-batch path runs
 }
 TUNED = {}
 # measured on B200 (N = 2^20): chain7 gradFD fp64 is compute-bound at 6 warps/SM
@@ -1776,7 +1779,7 @@ def _multi_knot_struct(model, alg, dt, name, progs, nx, over, tmem=0):
 
 
 def _ws_struct(model, alg, dt, warps, name=None, trees=None, zero_fill=True, fext=False, em=None, variants=0,
-               cluster=1):
+               cluster=1, progs=None, ext=None):
     """Device header of the warp-specialised mapping (see wsched.py).  With
     an `em` holding "imp" ops (split columns), the arena is the per-group
     slice of the split scratch the prefix kernel filled.  variants > 1: the
@@ -1790,19 +1793,19 @@ def _ws_struct(model, alg, dt, warps, name=None, trees=None, zero_fill=True, fex
     from . import wsched
     C = max(1, int(cluster))
     sw = warps * C  # warps the tasks are scheduled over
-    if variants and variants > 1 and em is None and trees is None:
+    if progs is not None:
+        pass  # explicit variant programs (wsched.split_programs)
+    elif variants and variants > 1 and em is None and trees is None:
         progs = wsched.variant_programs(model, alg, dt, variants, fext)
-    else:
-        progs = None
     if progs is not None and len(progs) > 1:
-        Ps = [wsched.plan(model, alg, dt, sw, em=e) for e in progs]
+        Ps = [wsched.plan(model, alg, dt, sw, em=e, ext=ext) for e in progs]
         P = dict(Ps[0])
         na = max(p["sched"].nslots for p in Ps)
         row = wsched.LANES * P["es"]
         P["arena_smem"] = row * (P["sin"] + na) <= wsched.SMEM_BUDGET
         P["stage"] = False
     else:
-        P = wsched.plan(model, alg, dt, sw, trees, zero_fill, fext, em=em)
+        P = wsched.plan(model, alg, dt, sw, trees, zero_fill, fext, em=em, ext=ext)
         Ps = [P]
         na = P["sched"].nslots
     if C > 1:
@@ -2034,6 +2037,30 @@ def _launch_unit(alg, dt, tag, K, text, rollout=False):
     ] + extra + [""])
 
 
+def _ws_split_unit(model, alg, dt, tag, K, tn):
+    """Small-batch split (wsched.split_programs) as two warp-specialised
+    kernels launched back to back: KA = the big tree's prefix (exports to a
+    per-device [N][nx] scratch, qdd), KB = CTA-row variants of its gradient
+    columns (the scratch as 4th input) and of the other root trees."""
+    from . import wsched
+    n = model.n_dof
+    pre, progs, nx = wsched.split_programs(model, alg, dt, int(tn["wsplit_groups"]))
+    ta, _, _ = _ws_struct(model, alg, dt, int(tn["wsplit_warps"]), K + "A", em=pre,
+                          ext=[nx, n if alg == "gradFD" else 0, 0])
+    tb, fl, L = _ws_struct(model, alg, dt, int(tn["wc_warps"]), K + "B", progs=progs)
+    maxn = int(tn["wsplit_max_n"])
+    unit = "\n".join([
+        ta.replace("#pragma once\n", ""), tb.replace("#pragma once\n", ""),
+        f'extern "C" int rbd__launch_{alg}_{dt}_{tag}(const void* q, const void* qd, const void* u, const void* fx,',
+        "                                void* o0, void* o1, void* o2, int64_t N, void* stream) {",
+        f"  (void)fx;",
+        f"  return rbd_launch_ws_split<{K}A, {K}B, {maxn}>(q, qd, u, o0, o1, o2, N, stream);",
+        "}",
+        "",
+    ])
+    return unit, fl, L
+
+
 def _big_part_unit(model, alg, dt, tag, K, tn, trees, zero_fill, fx):
     """A part whose one-knot program does not fit a thread.  Gradient
     programs are split (`split_columns`): a thread-per-knot prefix kernel
@@ -2118,8 +2145,15 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
                 X = "X" if fx else ""
                 tags = []
                 for mp in maps:
-                    tag = {"ws": "W", "fs": "F", "wc": "C"}.get(mp, "T") + X
+                    if mp == "wsplit" and (fx or alg not in ("gradID", "gradFD")):
+                        continue
+                    tag = {"ws": "W", "fs": "F", "wc": "C", "wsplit": "S"}.get(mp, "T") + X
                     K = f"Knot_{alg}_{dt}_{tag}"
+                    if mp == "wsplit":
+                        unit, fl, L = _ws_split_unit(model, alg, dt, tag, K, tn)
+                        files[f"k_{alg}_{dt}_{tag}.cu"] = unit
+                        tags.append(tag)
+                        continue
                     if mp == "wc":
                         text, fl, L = _ws_struct(model, alg, dt, int(tn["wc_warps"]), K, fext=fx,
                                                  variants=int(tn["wc_variants"]), cluster=int(tn["wc_cluster"]))
@@ -2199,6 +2233,9 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
                 if "wc" in maps:
                     # small batches: one knot group's tasks over a cluster / several CTA rows
                     pick = f"N <= {int(tn['wc_max_n'])} ? rbd__launch_{alg}_{dt}_C{X}{args} : ({pick})"
+                if "wsplit" in maps and not fx and alg in ("gradID", "gradFD"):
+                    # small batches of a big tree: prefix once, then the column variants
+                    pick = f"N <= {int(tn['wsplit_max_n'])} ? rbd__launch_{alg}_{dt}_S{args} : ({pick})"
                 dispatch += [
                     f'extern "C" int rbd__launch_{alg}_{dt}{"_fext" if fx else ""}(const void* q, const void* qd, '
                     "const void* u, const void* fx,",

@@ -833,6 +833,56 @@ static int rbd_launch_kernel(const void* q, const void* qd, const void* u, const
 }
 
 // ---------------------------------------------------------------------------
+// small-batch split (wsched.split_programs): KA = the big tree's prefix as a
+// warp-specialised kernel (exports -> a per-device [N][NX] scratch, the
+// tree's qdd -> out2), then KB = CTA-row variants of its gradient columns
+// (the scratch staged as their 4th input) and of the other root trees, on the
+// caller's stream.  The scratch is shared by every stream of the device:
+// launches are ordered by an event chain (as the warp-specialised global
+// arena); inside a stream capture the graph's order applies.
+// ---------------------------------------------------------------------------
+template <class KA, class KB, long long MAXN>
+static int rbd_launch_ws_split(const void* q, const void* qd, const void* u, void* o0, void* o1, void* o2,
+                               int64_t N, void* stream) {
+  typedef typename KA::T T;
+  static_assert(KB::NIN == 4, "column variants read the scratch as their 4th input");
+  if (N < 0 || N > MAXN) return RBD_EINVAL;
+  if (N == 0) return 0;
+  struct cache_t {
+    std::mutex lock;
+    T* scratch = nullptr;
+    cudaEvent_t last = nullptr;
+    bool used = false;
+  };
+  static cache_t cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cache_t& c = cache[dev & 63];
+  std::lock_guard<std::mutex> guard(c.lock);
+  cudaError_t e = cudaSuccess;
+  if (!c.scratch) {
+    e = cudaMalloc(&c.scratch, sizeof(T) * (size_t)MAXN * KA::E0);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.last, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      if (c.scratch) cudaFree(c.scratch);
+      c.scratch = nullptr;
+      return (int)e;
+    }
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool chain = !rbd_capturing(st);
+  if (chain && c.used && (e = cudaStreamWaitEvent(st, c.last, 0)) != cudaSuccess) return (int)e;
+  int rc = rbd_launch_kernel<KA>(q, qd, u, nullptr, c.scratch, KA::E1 ? o2 : nullptr, nullptr, N, stream);
+  if (rc == 0) rc = rbd_launch_kernel<KB>(q, qd, u, c.scratch, o0, o1, o2, N, stream);
+  if (rc == 0 && chain) {
+    e = cudaEventRecord(c.last, st);
+    if (e != cudaSuccess) return (int)e;
+    c.used = true;
+  }
+  return rc;
+}
+
+// ---------------------------------------------------------------------------
 // split gradient program (large root trees): the prefix kernel KA (thread per
 // knot: RNEA, articulated inertias, Minv, FD, RNEA at qdd) exports the values
 // the gradient columns need to a scratch; the column kernel KB (thread per

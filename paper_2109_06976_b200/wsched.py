@@ -309,8 +309,81 @@ def variant_programs(model, alg, dtype, k, fext=False):
     return progs
 
 
-def plan(model, alg, dtype, warps, trees=None, zero_fill=True, fext=False, em=None):
-    """Schedule + memory plan of the warp-specialised kernel."""
+def split_programs(model, alg, dtype, k, big_tree=0):
+    """Small-batch split of a gradient program (two warp-specialised
+    launches): kernel A runs the big tree's prefix (RNEA, articulated
+    inertias, Minv, FD, RNEA at qdd) once per knot group and stores the values
+    the gradient columns import as its output 0 (a [N][nx] scratch) and the
+    tree's qdd as output 1; kernel B's CTA-row variants are the big tree's
+    gradient columns in ~k groups -- the scratch is their 4th input, so an
+    import is an ordinary (re-materialised) load of the staged row -- plus
+    the other root trees' whole programs.  All of B's variants share one
+    input layout (q, qd, u, scratch) and sin/cos table; cross-tree zeros are
+    stored round robin.  Returns (prefix em, [variant ems], nx)."""
+    n = model.n_dof
+    trees = [model.subtree(r) for r in model.roots()]
+    em = cg.generate_knot(model, alg, dtype, trees=(big_tree,), zero_fill=False, full_window=True)
+    pre, cols, nx = cg.split_columns(em)
+    # prefix: exports -> output 0 (scratch), qdd (gradFD output 2) -> output 1
+    pops, ptasks = [], []
+    for op, t in zip(pre.ops, pre.tasks):
+        if op[0] == "xst":
+            op = ("st", 0, op[1], op[2])
+        elif op[0] == "st":
+            if op[1] != 2:
+                raise cg.GenerationError("split prefix stores only qdd")
+            op = ("st", 1, op[2], op[3])
+        pops.append(op)
+        ptasks.append(t)
+    prefix = cg._sub_emit(pre, pops, ptasks)
+
+    def with_scratch_input(e):
+        """append the scratch row as the 4th input (after u); sin/cos follow it"""
+        e.in_layout = list(e.in_layout) + [("x", e.in_total, nx, 0, nx)]
+        e.in_total = e.in_total + nx
+        return e
+
+    base = em.in_total  # the scratch row starts after q, qd, u
+    gtasks = list(dict.fromkeys(t for t in cols.tasks if t.startswith("grad.")))
+    g = max(1, min(int(k), len(gtasks)))
+    # LPT: column tasks by op count onto the least-loaded group (a column's
+    # cost grows with its subtree: column 0 of the torso spans every frame)
+    cost = {t: 0 for t in gtasks}
+    for t in cols.tasks:
+        if t in cost:
+            cost[t] += 1
+    groups, load = [set() for _ in range(g)], [0] * g
+    for t in sorted(gtasks, key=lambda x: (-cost[x], x)):
+        j = min(range(g), key=lambda i: (load[i], i))
+        groups[j].add(t)
+        load[j] += cost[t]
+    variants = []
+    for grp in groups:
+        ops, tasks = [], []
+        for op, t in zip(cols.ops, cols.tasks):
+            if op[0] == "imp":
+                ops.append(("ld", op[1], base + op[2]))
+                tasks.append("in")
+            elif t in ("in", "xf") or t in grp:
+                ops.append(op)
+                tasks.append(t)
+        variants.append(with_scratch_input(cg._sub_emit(cols, ops, tasks)))
+    for t in range(len(trees)):
+        if t != big_tree:
+            variants.append(with_scratch_input(cg.generate_knot(model, alg, dtype, trees=(t,), zero_fill=False,
+                                                                full_window=True)))
+    stored = {(op[1], op[2]) for e in variants for op in e.ops if op[0] == "st"}
+    zeros = [(o, idx) for o in (0, 1) for idx in range(n * n) if (o, idx) not in stored]
+    for z, (o, idx) in enumerate(zeros):
+        e = variants[z % len(variants)]
+        e.ops.append(("st", o, idx, 0.0))
+        e.tasks.append("zeros")
+    return prefix, variants, nx
+
+
+def plan(model, alg, dtype, warps, trees=None, zero_fill=True, fext=False, em=None, ext=None):
+    """Schedule + memory plan of the warp-specialised kernel (ext: output
+    extents when they differ from the algorithm's, e.g. a split prefix)."""
     if em is None:
         em = cg.generate_knot(model, alg, dtype, trees, zero_fill, fext=fext)
     sched = Schedule(em, warps)
@@ -319,8 +392,9 @@ def plan(model, alg, dtype, warps, trees=None, zero_fill=True, fext=False, em=No
     es = 8 if dtype == "f64" else 4
     nin = len(em.in_layout)
     nsc = sum(1 for op in em.ops if op[0] == "sincos")
-    ext = [e for _, e in cg.outputs(alg, n)]
-    ext += [0] * (3 - len(ext))
+    if ext is None:
+        ext = [e for _, e in cg.outputs(alg, n)]
+    ext = list(ext) + [0] * (3 - len(ext))
     sin = em.in_total + 2 * nsc
     row = LANES * es
     sout = sum(ext)

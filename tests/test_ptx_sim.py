@@ -57,13 +57,13 @@ def run_ws(model, alg, dt, x, warps, arena_space="shared", out_space="shared", f
     P = wsched.plan(model, alg, dt, warps, fext=fext, em=em)
     S = P["sched"]
     n = P["n"]
-    nin = P["em"].in_total // n
+    base = P["em"].in_total  # inputs (3 or 4 arrays, or f_ext) then sin/cos
     es = 8 if dt == "f64" else 4
     L = wsched.LANES
     row = {i: float(v) for i, v in enumerate(x)}
     for k, slot in enumerate(_sincos_slots(P["em"])):
-        row[nin * n + 2 * k] = math.sin(x[slot])
-        row[nin * n + 2 * k + 1] = math.cos(x[slot])
+        row[base + 2 * k] = math.sin(x[slot])
+        row[base + 2 * k + 1] = math.cos(x[slot])
     arena = {}
     outs = [dict() for _ in range(3)] if outs is None else outs
     astride = L * es if arena_space == "shared" else 32 * es
@@ -72,7 +72,7 @@ def run_ws(model, alg, dt, x, warps, arena_space="shared", out_space="shared", f
     for phase in S.phases:
         for tasks in phase:
             if tasks:
-                lines = wsched.ptx_block(S, tasks, dt, nin * n, nin * n, arena_space, out_space, 0, ctab)
+                lines = wsched.ptx_block(S, tasks, dt, base, base, arena_space, out_space, 0, ctab)
                 ptxsim.run_block(lines, [row, arena] + outs + [None], [L * es, astride, ostride, ostride, ostride],
                                  f32=(dt == "f32"), consts={"K": sorted(ctab.index, key=ctab.index.get)})
     return [np.array([o.get(i, np.nan) for i in range(e)]) for o, (_, e) in zip(outs, codegen.outputs(alg, n))], S
@@ -173,6 +173,33 @@ def test_ws_cluster_arena(name, C):
             got = np.array([o.get(i, np.nan) for i in range(e)])
             assert np.all(np.isfinite(got)), (name, alg, nm, "unwritten output")
             assert rel_err(got[None], g[f"{alg}.{nm}"][1:2]) < 1e-12, (name, alg, nm)
+
+
+@pytest.mark.parametrize("name,alg", [("humanoid30", "gradFD"), ("humanoid30", "gradID"), ("quad12", "gradFD")])
+def test_ws_split_programs(name, alg):
+    """Small-batch split: the prefix program's outputs (the [nx] export row
+    and the tree's qdd) feed the column variants as their 4th input; with
+    the other trees' variants they write every output element once and match
+    the reference."""
+    g = golden(name)
+    m = models.load(name)
+    n = m.n_dof
+    pre, progs, nx = wsched.split_programs(m, alg, "f64", 4)
+    x = _inputs(g, alg, 2, n)
+    scratch, outs = {}, [dict() for _ in range(3)]
+    pouts = [scratch, outs[2], {}]  # prefix: output 0 = exports, output 1 = qdd
+    run_ws(m, alg, "f64", x, 6, out_space="global", em=pre, outs=pouts)
+    assert len(scratch) == nx
+    stores = [(op[1], op[2]) for e in progs for op in e.ops if op[0] == "st"]
+    assert len(stores) == len(set(stores))
+    xs = np.concatenate([x, [scratch[i] for i in range(nx)]])
+    for e in progs:
+        assert len(e.in_layout) == 4
+        run_ws(m, alg, "f64", xs, 5, out_space="global", em=e, outs=outs)
+    for (nm, e), o in zip(codegen.outputs(alg, n), outs):
+        got = np.array([o.get(i, np.nan) for i in range(e)])
+        assert np.all(np.isfinite(got)), (name, alg, nm, "unwritten output")
+        assert rel_err(got[None], g[f"{alg}.{nm}"][2:3]) < 1e-12, (name, alg, nm)
 
 
 def test_ws_schedule_properties():
