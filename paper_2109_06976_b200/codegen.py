@@ -817,7 +817,13 @@ for _a in ALGORITHMS:
             # 8 warps; measured gradFD N=256 fp64 95 -> 41 us, fp32 63 -> 36 us,
             # N=1024 fp64 98 -> 83 us (slower than one CTA per group from 4096)
             TUNED[("humanoid30", _a, _d)].update({"maps": ["ws", "wc"], "wc_warps": 8, "wc_variants": 10,
-                                                  "wc_max_n": 1024})
+                                                  "wc_max_n": 256})
+            if _d == "f64":
+                # 256 < N <= 1024: the split (prefix kernel of 8 warps, then 6
+                # column groups + the legs): N=1024 82.6 -> 66.8 us; slower
+                # than the variants below (N=256: 37.7 vs 36.2 us)
+                TUNED[("humanoid30", _a, _d)].update({"maps": ["ws", "wc", "wsplit"], "wsplit_max_n": 1024,
+                                                      "wsplit_warps": 8})
         # the fused rollout runs the one-CTA warp-specialised program (no
         # CTA-row variants: a step's Euler update needs all of a group's
         # outputs); measured B=128 x 32 steps gradFD fp64: fused 2.80 ms vs
@@ -2230,12 +2236,12 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
                 if "fs" in maps:
                     # small batches: the fine-grained schedule (lowest latency)
                     pick = f"N <= {int(tn['fs_max_n'])} ? rbd__launch_{alg}_{dt}_F{X}{args} : ({pick})"
+                if "wsplit" in maps and not fx and alg in ("gradID", "gradFD"):
+                    # mid-size batches of a big tree: prefix once, then the column variants
+                    pick = f"N <= {int(tn['wsplit_max_n'])} ? rbd__launch_{alg}_{dt}_S{args} : ({pick})"
                 if "wc" in maps:
                     # small batches: one knot group's tasks over a cluster / several CTA rows
                     pick = f"N <= {int(tn['wc_max_n'])} ? rbd__launch_{alg}_{dt}_C{X}{args} : ({pick})"
-                if "wsplit" in maps and not fx and alg in ("gradID", "gradFD"):
-                    # small batches of a big tree: prefix once, then the column variants
-                    pick = f"N <= {int(tn['wsplit_max_n'])} ? rbd__launch_{alg}_{dt}_S{args} : ({pick})"
                 dispatch += [
                     f'extern "C" int rbd__launch_{alg}_{dt}{"_fext" if fx else ""}(const void* q, const void* qd, '
                     "const void* u, const void* fx,",
@@ -2295,7 +2301,8 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
                     nin, ext, es = table[(alg, dt, fx)]
                     fn = f"rbd__launch_{alg}_{dt}{'_fext' if fx else ''}"
                     tn = tuning(model, alg, dt)
-                    cmax = int(tn["wc_max_n"]) if "wc" in tn["maps"] else 0
+                    cmax = max(int(tn["wc_max_n"]) if "wc" in tn["maps"] else 0,
+                               int(tn["wsplit_max_n"]) if "wsplit" in tn["maps"] and not fx else 0)
                     pair.append(f"{{&{fn}, {nin}, {ext[0]}, {ext[1]}, {ext[2]}, {es}, {cmax}}}")
                 else:
                     pair.append("{nullptr, 0, 0, 0, 0, 0, 0}")

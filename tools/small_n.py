@@ -57,7 +57,7 @@ def main():
                 outs = [torch.empty((N, e), dtype=tdt, device="cuda") for _, e in codegen.outputs(alg, n)]
                 ptr = [x.data_ptr() for x in xs] + [0] + [o.data_ptr() for o in outs] + [0] * (3 - len(outs))
                 rec = {"robot": robot, "alg": alg, "dtype": dt, "N": N}
-                for tag in ("C", "F", "W", "T", ""):
+                for tag in ("S", "C", "F", "W", "T", ""):
                     name = f"rbd__launch_{alg}_{dt}_{tag}" if tag else f"rbd__launch_{alg}_{dt}"
                     try:
                         f = getattr(lib, name)
