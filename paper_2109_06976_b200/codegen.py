@@ -793,7 +793,11 @@ for _a in ALGORITHMS:
         # thread-per-knot kernel runs at ~80% of HBM bandwidth at N = 2^20
         # (3.4x the warp-specialised one); humanoid30's one-knot program
         # (~600 live values) does not fit a thread
-        TUNED[("quad12", _a, _d)] = {"warps": 16, "minb": 1, "ws_max_n": 4096}  # thread ahead from 8192
+        TUNED[("quad12", _a, _d)] = {"warps": 16, "minb": 1, "ws_max_n": 4096,  # thread ahead from 8192
+                                     # host path, small N: the one-CTA kernel stages its outputs and writes
+                                     # them coalesced over PCIe (gradFD N=128 fp64: 23 us with I/O) --
+                                     # faster than the variants + a device->host copy (40 us)
+                                     "zc_variants": False}
         if _a in ("gradID", "gradFD"):
             # small batches: CTA-row variants (per leg x column group) spread a
             # 32-knot group over 8 SMs; measured gradFD N=128 fp64 6.2 -> 4.4 us,
@@ -2140,6 +2144,7 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
     files, flops, table = {}, {}, {}
     dispatch = []
     rollouts = set()
+    zc_direct = {}  # (alg, dt, fext) -> the host path's small-batch launcher stages its outputs
     sig = "(const void*, const void*, const void*, const void*, void*, void*, void*, int64_t, void*);"
     args = "(q, qd, u, fx, o0, o1, o2, N, stream)"
     for alg in algorithms:
@@ -2236,19 +2241,33 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
                 if "fs" in maps:
                     # small batches: the fine-grained schedule (lowest latency)
                     pick = f"N <= {int(tn['fs_max_n'])} ? rbd__launch_{alg}_{dt}_F{X}{args} : ({pick})"
+                # the small-batch host path (zero-copy outputs into pinned host
+                # memory) prefers kernels that stage their outputs (coalesced
+                # PCIe writes) when the robot's tuning says so ("zc_variants")
+                host_pick = pick
                 if "wsplit" in maps and not fx and alg in ("gradID", "gradFD"):
                     # mid-size batches of a big tree: prefix once, then the column variants
                     pick = f"N <= {int(tn['wsplit_max_n'])} ? rbd__launch_{alg}_{dt}_S{args} : ({pick})"
+                if not tn.get("zc_variants", True):
+                    host_pick = pick
                 if "wc" in maps:
                     # small batches: one knot group's tasks over a cluster / several CTA rows
                     pick = f"N <= {int(tn['wc_max_n'])} ? rbd__launch_{alg}_{dt}_C{X}{args} : ({pick})"
+                if tn.get("zc_variants", True):
+                    host_pick = pick
                 dispatch += [
                     f'extern "C" int rbd__launch_{alg}_{dt}{"_fext" if fx else ""}(const void* q, const void* qd, '
                     "const void* u, const void* fx,",
                     "                                void* o0, void* o1, void* o2, int64_t N, void* stream) {",
                     f"  return {pick};",
                     "}",
+                    f'extern "C" int rbd__launch_{alg}_{dt}{"_fext" if fx else ""}_host(const void* q, const void* qd, '
+                    "const void* u, const void* fx,",
+                    "                                void* o0, void* o1, void* o2, int64_t N, void* stream) {",
+                    f"  return {host_pick};",
+                    "}",
                 ]
+                zc_direct[(alg, dt, fx)] = host_pick != pick
             dispatch += [
                 f'extern "C" int rbd_{alg}_{dt}(const {T}* q, const {T}* qd, const {T}* u, {T}* o0,',
                 f"                         {T}* o1, {T}* o2, int64_t N, void* stream) {{",
@@ -2303,9 +2322,11 @@ def generate_sources(model, algorithms=ALGORITHMS, dtypes=DTYPES):
                     tn = tuning(model, alg, dt)
                     cmax = max(int(tn["wc_max_n"]) if "wc" in tn["maps"] else 0,
                                int(tn["wsplit_max_n"]) if "wsplit" in tn["maps"] and not fx else 0)
-                    pair.append(f"{{&{fn}, {nin}, {ext[0]}, {ext[1]}, {ext[2]}, {es}, {cmax}}}")
+                    if zc_direct.get((alg, dt, fx)):
+                        cmax = 0  # the host launcher runs output-staging kernels: zero-copy outputs
+                    pair.append(f"{{&{fn}, {nin}, {ext[0]}, {ext[1]}, {ext[2]}, {es}, {cmax}, &{fn}_host}}")
                 else:
-                    pair.append("{nullptr, 0, 0, 0, 0, 0, 0}")
+                    pair.append("{nullptr, 0, 0, 0, 0, 0, 0, nullptr}")
             row.append("{" + ", ".join(pair) + "}")
         main.append("    {" + ", ".join(row) + "},")
     main += [

@@ -87,6 +87,14 @@ __host__ __device__ constexpr int rbd_nprog() { return rbd_prog_traits<K>::nprog
 
 template <class K>
 __host__ __device__ constexpr int rbd_nout() { return rbd_park_traits<K>::nout; }
+// widest per-knot input window of a kernel's inputs (registers for staging)
+template <class K>
+__host__ __device__ constexpr int rbd_max_inw() {
+  int w = 0;
+  for (int a = 0; a < K::NIN; ++a) w = K::inw(a) > w ? K::inw(a) : w;
+  return w;
+}
+
 template <class K>
 __host__ __device__ constexpr bool rbd_ofull() { return rbd_park_traits<K>::ofull; }
 
@@ -264,7 +272,7 @@ rbd_ws_kernel(const typename K::T* __restrict__ q, const typename K::T* __restri
     const long long base = g * 32;
     const int nk = (N - base) < 32 ? (int)(N - base) : 32;
     // input a: 32 knots x inw(a) scalars, PER(a) loads per thread, all in flight
-    constexpr int WMAX = 6 * K::NP;
+    constexpr int WMAX = rbd_max_inw<K>();  // widest input row (f_ext 6 per dof, a split scratch nx)
     constexpr int PMAX = (32 * WMAX + NT - 1) / NT;
     T v[K::NIN][PMAX];
 #pragma unroll
@@ -364,7 +372,7 @@ rbd_fs_kernel(const typename K::T* __restrict__ q, const typename K::T* __restri
   for (long long g = blockIdx.x; g < groups; g += gridDim.x) {
     const long long base = g * 32;
     const int nk = (N - base) < 32 ? (int)(N - base) : 32;
-    constexpr int WMAX = 6 * K::NP;
+    constexpr int WMAX = rbd_max_inw<K>();  // widest input row (f_ext 6 per dof, a split scratch nx)
     constexpr int PMAX = (32 * WMAX + NT - 1) / NT;
     T v[K::NIN][PMAX];
 #pragma unroll
@@ -618,7 +626,7 @@ rbd_wc_kernel(const typename K::T* __restrict__ q, const typename K::T* __restri
   for (long long g = blockIdx.x / K::C; g < groups; g += ncl) {
     const long long base = g * 32;
     const int nk = (N - base) < 32 ? (int)(N - base) : 32;
-    constexpr int WMAX = 6 * K::NP;
+    constexpr int WMAX = rbd_max_inw<K>();  // widest input row (f_ext 6 per dof, a split scratch nx)
     constexpr int PMAX = (32 * WMAX + NT - 1) / NT;
     T v[K::NIN][PMAX];
 #pragma unroll
@@ -1025,6 +1033,7 @@ struct rbd_entry {
   int64_t copy_out_max_n;  // batches up to this size run a kernel whose output stores are not
                            // coalesced (CTA-row variants): the small-batch host path lands its
                            // outputs in device memory and copies them back once
+  rbd_launch_fn fn_host;   // the small-batch host path's launcher (may prefer output-staging kernels)
 };
 #if defined(RBD_MAIN_TU)
 static const rbd_entry* rbd_entry_for(int alg, int dtype, int fext);  // generated main TU
@@ -1219,7 +1228,7 @@ static int rbd_run_host_impl(rbd_session* s, int alg, int dtype, const void* q, 
       }
     }
     cudaStream_t st = s->stream[0];
-    rc = e->fn(din[0], din[1], din[2], din[3], dout[0], dout[1], dout[2], N, (void*)st);
+    rc = e->fn_host(din[0], din[1], din[2], din[3], dout[0], dout[1], dout[2], N, (void*)st);
     unsigned char* ho = s->hstage + rbd_align256(in_bytes) + 4 * 256;  // after the staged inputs
     if (rc == 0 && via_device) {
       if (direct_out) {
