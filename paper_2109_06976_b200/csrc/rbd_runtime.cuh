@@ -98,6 +98,41 @@ __host__ __device__ constexpr int rbd_max_inw() {
 template <class K>
 __host__ __device__ constexpr bool rbd_ofull() { return rbd_park_traits<K>::ofull; }
 
+// coalesced write-back of nk knots x E elements of one output array, 16-byte
+// streaming stores when E is a multiple of the vector width and dst is
+// 16-byte aligned (else 8/4-byte stores); get(k, e) yields knot k's element e
+template <class T>
+struct rbd_vec16;
+template <>
+struct rbd_vec16<double> {
+  typedef double2 t;
+};
+template <>
+struct rbd_vec16<float> {
+  typedef float4 t;
+};
+template <class T, int E, int NT, class F>
+__device__ __forceinline__ void rbd_write_back(T* dst, int nk, int tid, F get) {
+  constexpr int VW = 16 / (int)sizeof(T);
+  if (E % VW == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    typedef typename rbd_vec16<T>::t V;
+    V* vd = reinterpret_cast<V*>(dst);
+    for (int p = tid; p < nk * (E / VW); p += NT) {
+      const int idx = p * VW, k = idx / E, e = idx - k * E;
+      V v;
+      T* pv = reinterpret_cast<T*>(&v);
+#pragma unroll
+      for (int j = 0; j < VW; ++j) pv[j] = get(k, e + j);
+      __stcs(vd + p, v);
+    }
+  } else {
+    for (int idx = tid; idx < nk * E; idx += NT) {
+      const int k = idx / E, e = idx - k * E;
+      __stcs(dst + idx, get(k, e));
+    }
+  }
+}
+
 template <class K>
 __global__ void __launch_bounds__(K::BK, K::MINB)
 rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __restrict__ qd,
@@ -193,45 +228,27 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
         else
           __stcs(o2 + (base + k) * K::E2 + (e - K::E0 - K::E1), v);
       }
-    } else
-#pragma unroll
-    for (int b = 0; b < 3; ++b) {
-      const int E = b == 0 ? K::E0 : (b == 1 ? K::E1 : K::E2);
-      const int off = b == 0 ? 0 : (b == 1 ? K::E0 : K::E0 + K::E1);
-      if (E == 0) continue;
-      T* dst = (b == 0 ? o0 : (b == 1 ? o1 : o2)) + base * E;
-      for (int idx = tid; idx < nk * E; idx += BK) {
-        const int k = idx / E, e = idx - k * E;
-        const int sl = s_map[off + e];
-        __stcs(dst + idx, sl >= 0 ? s_in[k * K::SIN + sl] : T(0));
-      }
+    } else {
+      auto from_map = [&](int off) {
+        return [=](int k, int e) {
+          const int sl = s_map[off + e];
+          return sl >= 0 ? s_in[k * K::SIN + sl] : T(0);
+        };
+      };
+      rbd_write_back<T, K::E0, BK>(o0 + base * K::E0, nk, tid, from_map(0));
+      if constexpr (K::E1 > 0) rbd_write_back<T, K::E1, BK>(o1 + base * K::E1, nk, tid, from_map(K::E0));
+      if constexpr (K::E2 > 0)
+        rbd_write_back<T, K::E2, BK>(o2 + base * K::E2, nk, tid, from_map(K::E0 + K::E1));
     }
   } else if constexpr (K::STAGE) {
     T* o = s_out + tid * K::SOUT;
     K::run_dev(my, o, o + K::E0, o + K::E0 + K::E1, 1u, xb, tm);
     __syncthreads();
     // coalesced write-back, one output array at a time
-    {
-      T* dst = o0 + base * K::E0;
-      for (int idx = tid; idx < nk * K::E0; idx += BK) {
-        const int k = idx / K::E0, e = idx - k * K::E0;
-        __stcs(dst + idx, s_out[k * K::SOUT + e]);
-      }
-    }
-    if constexpr (K::E1 > 0) {
-      T* dst = o1 + base * K::E1;
-      for (int idx = tid; idx < nk * K::E1; idx += BK) {
-        const int k = idx / K::E1, e = idx - k * K::E1;
-        __stcs(dst + idx, s_out[k * K::SOUT + K::E0 + e]);
-      }
-    }
-    if constexpr (K::E2 > 0) {
-      T* dst = o2 + base * K::E2;
-      for (int idx = tid; idx < nk * K::E2; idx += BK) {
-        const int k = idx / K::E2, e = idx - k * K::E2;
-        __stcs(dst + idx, s_out[k * K::SOUT + K::E0 + K::E1 + e]);
-      }
-    }
+    auto staged = [&](int off) { return [=](int k, int e) { return s_out[k * K::SOUT + off + e]; }; };
+    rbd_write_back<T, K::E0, BK>(o0 + base * K::E0, nk, tid, staged(0));
+    if constexpr (K::E1 > 0) rbd_write_back<T, K::E1, BK>(o1 + base * K::E1, nk, tid, staged(K::E0));
+    if constexpr (K::E2 > 0) rbd_write_back<T, K::E2, BK>(o2 + base * K::E2, nk, tid, staged(K::E0 + K::E1));
   } else {
     // every thread runs the program (CTA barriers inside); stores of the
     // padding threads of the last CTA are predicated off
