@@ -71,14 +71,14 @@ class Session:
         self.handle = h
 
     def run(self, alg, dtype, in_arrays, out_arrays, N, f_ext=None):
-        ins = [a.ctypes.data_as(ctypes.c_void_p) for a in in_arrays] + [None] * (3 - len(in_arrays))
-        outs = [a.ctypes.data_as(ctypes.c_void_p) for a in out_arrays] + [None] * (3 - len(out_arrays))
+        ins = [a.ctypes.data for a in in_arrays] + [None] * (3 - len(in_arrays))
+        outs = [a.ctypes.data for a in out_arrays] + [None] * (3 - len(out_arrays))
         if f_ext is not None:
             rc = self.lib.rbd_run_host_fext(self.handle, _ALG_ID[alg], _DT_ID[dtype], *ins,
-                                            f_ext.ctypes.data_as(ctypes.c_void_p), *outs, ctypes.c_int64(N))
+                                            f_ext.ctypes.data, *outs, N)
             check(rc, f"rbd_run_host_fext({alg}, {dtype})")
             return
-        rc = self.lib.rbd_run_host(self.handle, _ALG_ID[alg], _DT_ID[dtype], *ins, *outs, ctypes.c_int64(N))
+        rc = self.lib.rbd_run_host(self.handle, _ALG_ID[alg], _DT_ID[dtype], *ins, *outs, N)
         check(rc, f"rbd_run_host({alg}, {dtype})")
 
     def bench(self, alg, dtype, in_arrays, out_arrays, N, reps):
