@@ -784,6 +784,12 @@ TUNED[("chain7", "gradFD", "f64")].update({"tmem_row": True, "prefetch_dist": 24
 # 32-knot CTAs: finer-grained CTA turnover (staging / write-back barriers),
 # measured 1.35 -> 1.22 ms (fp64) and 0.64 -> 0.60 ms (fp32) at N = 2^20
 TUNED[("chain7", "gradFD", "f32")] = {"bk": 32}
+# rollouts (B=128, H=64, gradFD fp64): per-step launches replayed from a graph
+# 0.71 ms vs the fused kernel 0.76 ms (equal at B=4096); quad12 fused 0.32 vs
+# 0.40 ms keeps the default
+for _a in ("FD", "gradFD"):
+    for _d in DTYPES:
+        TUNED.setdefault(("chain7", _a, _d), {})["rollout_fused"] = False
 # the fine-grained schedule ("fs", fsched.py) measured slower than the task
 # schedule at every small N for chain7 (gradFD fp64 N=128: 10.7 vs 9.9 us;
 # ID: 3.4 vs 2.9 us; profiles/small_n_r2.md), so no robot compiles it by default

@@ -489,15 +489,17 @@ rbd_ws_rollout_kernel(typename K::T* __restrict__ q, typename K::T* __restrict__
   for (long long g = blockIdx.x; g < groups; g += gridDim.x) {
     const long long base = g * 32;
     const int nk = (B - base) < 32 ? (int)(B - base) : 32;
-    for (int k = 0; k < H; ++k) {
-      const size_t st = (size_t)k * B * n;
-      const T* src3[3] = {q + st, qd + st, tau + st};
+    {  // step 0: q_0, qd_0, tau_0; later steps keep q, qd in shared memory
+      const T* src3[3] = {q, qd, tau};
       for (int a = 0; a < 3; ++a)
         for (int idx = tid; idx < 32 * n; idx += NT) {
           const int kn = idx / n, j = idx - kn * n;
           s_in[(K::inr(a) + j) * L + kn] = kn < nk ? src3[a][(base + kn) * n + j] : T(0);
         }
       __syncthreads();
+    }
+    for (int k = 0; k < H; ++k) {
+      const size_t st = (size_t)k * B * n;
       K::prologue(s_in, warp, lane);
       __syncthreads();
       const unsigned a_in = (unsigned)__cvta_generic_to_shared(s_in + lane);
@@ -521,6 +523,18 @@ rbd_ws_rollout_kernel(typename K::T* __restrict__ q, typename K::T* __restrict__
         a2 = (unsigned long long)(p2 + (base + kk) * K::E2);
       }
       K::run_group(0, warp, a_in, a_ar, a0, a1, a2, lane < nk ? 1u : 0u);  // ends with a barrier
+      // the program is done with tau_k: fetch tau_{k+1} into its rows with
+      // asynchronous copies that land under the write-back and the Euler update
+      if (k + 1 < H) {
+        const T* tn = tau + (size_t)(k + 1) * B * n;
+        for (int idx = tid; idx < nk * n; idx += NT) {
+          const int kn = idx / n, j = idx - kn * n;
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(s_in + (K::inr(2) + j) * L + kn);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(sa), "l"(tn + (base + kn) * n + j),
+                       "n"((int)sizeof(T)) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
       if constexpr (K::STAGE) {
         for (int b = 0; b < 3; ++b) {
           const int E = b == 0 ? K::E0 : (b == 1 ? K::E1 : K::E2);
@@ -533,16 +547,24 @@ rbd_ws_rollout_kernel(typename K::T* __restrict__ q, typename K::T* __restrict__
         }
       }
       __syncthreads();  // this step's qdd (global or staged) is visible to the whole CTA
+      // semi-implicit Euler from the staged states; the new states go to the
+      // trajectory (global) and stay in shared memory for the next step
       const T* qddk = (K::E2 ? p2 : p0) + base * n;
       const size_t nx = (size_t)(k + 1) * B * n;
       for (int idx = tid; idx < nk * n; idx += NT) {
         const int kn = idx / n, j = idx - kn * n;
         const T a = K::STAGE ? s_out[((K::E2 ? K::E0 + K::E1 : 0) + j) * L + kn] : qddk[idx];
-        const T v = qd[st + (base + kn) * n + j] + dt * a;
+        T& sq = s_in[(K::inr(0) + j) * L + kn];
+        T& sqd = s_in[(K::inr(1) + j) * L + kn];
+        const T v = sqd + dt * a;
+        const T qn = sq + dt * v;
+        sqd = v;
+        sq = qn;
         qd[nx + (base + kn) * n + j] = v;
-        q[nx + (base + kn) * n + j] = q[st + (base + kn) * n + j] + dt * v;
+        q[nx + (base + kn) * n + j] = qn;
       }
-      __syncthreads();  // next step stages the new states
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();  // states and tau_{k+1} staged for the next step
     }
   }
 }

@@ -67,7 +67,7 @@ def test_rollout_fp32():
     rng = np.random.default_rng(5)
     q0, qd0 = rng.uniform(-1, 1, (B, n)).astype(np.float32), rng.uniform(-1, 1, (B, n)).astype(np.float32)
     tau = rng.uniform(-1, 1, (B, H, n)).astype(np.float32)
-    r = Rollout(m, B, H, dt, "f32", grad=False, graph=True)
+    r = Rollout(m, B, H, dt, "f32", grad=False, graph=True, fused=True)  # the fused FD kernel in fp32
     r.run(torch.from_numpy(q0).cuda(), torch.from_numpy(qd0).cuda(), torch.from_numpy(tau).cuda())
     torch.cuda.synchronize()
     q, qd, qdd = (x.cpu().numpy().astype(np.float64) for x in r.trajectories())
