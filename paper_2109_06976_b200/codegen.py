@@ -449,13 +449,47 @@ class _Program:
             if em.fext:
                 add_t(rows, self.inp["f_ext"][i], -1.0)  # f_i -= f_ext_i (refdyn.py:79-80)
             f[i] = em.vec(rows, hint="f")
+        f_local = dict(f)  # per-link forces before the backward accumulation
         tau = {}
         for i in reversed(tree):
             tau[i] = em.lin([(1.0, f[i][r], self.S[i][r]) for r in range(6)], hint="tau")
             p = self.parent[i]
             if p >= 0:
                 f[p] = em.vec(add_t(self.xtf(i, f[i]), f[p]), hint="f")
-        return dict(v=v, a=a, f=f, Xv=Xv, Xa=Xa, vJ=vJ, Iv=Iv, tau=tau)
+        return dict(v=v, a=a, f=f, Xv=Xv, Xa=Xa, vJ=vJ, Iv=Iv, tau=tau, f_local=f_local)
+
+    def emit_rnea_delta(self, tree, qdd, R0):
+        """RNEA at qdd from the RNEA at qdd = 0 of the same (q, qd) (R0):
+        the accelerations differ by da_i = X_i da_p + S_i qdd_i -- gravity and
+        the velocity-product terms cancel -- so the link forces are
+        f_i = f0_i + I_i da_i before the backward pass, and X_i a_p = X_i a0_p
+        + X_i da_p.  Same values as emit_rnea(tree, qdd) (refdyn.py:55-88) up
+        to rounding, without re-forming I v, v x* I v and v x vJ."""
+        em = self.em
+        base = em.task
+        da, Xa, f = {}, {}, {}
+        for i in tree:
+            p = self.parent[i]
+            rows = _rows()
+            Xda = em.vec(self.xm(i, da[p]), hint="xda") if p >= 0 and p in da else None
+            if Xda is not None:
+                add_t(rows, Xda)
+            if qdd[i] is not None:
+                for r in range(6):
+                    rows[r].append((1.0, qdd[i], self.S[i][r]))
+            da[i] = em.vec(rows, hint="da")
+            Xa[i] = em.vec(add_t(_rows_from(R0["Xa"][i]), Xda), hint="a") if Xda is not None else R0["Xa"][i]
+            rows = mv_t(self.I[i], da[i])
+            add_t(rows, R0["f_local"][i])
+            f[i] = em.vec(rows, hint="f")
+        tau = {}
+        for i in reversed(tree):
+            tau[i] = em.lin([(1.0, f[i][r], self.S[i][r]) for r in range(6)], hint="tau")
+            p = self.parent[i]
+            if p >= 0:
+                f[p] = em.vec(add_t(self.xtf(i, f[i]), f[p]), hint="f")
+        em.task = base
+        return dict(v=R0["v"], a=None, f=f, Xv=R0["Xv"], Xa=Xa, vJ=R0["vJ"], Iv=R0["Iv"], tau=tau)
 
     # -- direct Minv (reference refdyn.py:128-169, column-wise) ------------------
     def emit_minv(self, tree, t=0, store=False, on_column=None):
@@ -659,7 +693,10 @@ class _Program:
                     for i in tree:
                         self.store("o2", i, qdd[i])
                 em.task = f"rnea1.{t}"
-                R = self.emit_rnea(tree, qdd, v_in=None if self.lowmem else (R0["v"], R0["Xv"]))
+                if self.lowmem:
+                    R = self.emit_rnea(tree, qdd)  # fewer values live across the Minv/FD phase
+                else:
+                    R = self.emit_rnea_delta(tree, qdd, R0)
                 self.emit_xcf(tree, R)
                 for o, kind in (("o0", "q"), ("o1", "qd")):
                     for c in tree:

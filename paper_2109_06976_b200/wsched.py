@@ -102,6 +102,15 @@ class Schedule:
 
         for t in self.task_ops:
             lv(t)
+        # sink tasks (nothing depends on them: gradient columns, output-only
+        # tasks) go to the last phase, so an early-ready sink (a q-dot column
+        # that needs no RNEA at qdd) does not lengthen a middle phase
+        if level:
+            last = max(level.values())
+            has_user = {d for t in self.task_ops for d in deps[t]}
+            for t in self.task_ops:
+                if t not in has_user:
+                    level[t] = last
         self.level = level
         nphase = 1 + max(level.values()) if level else 0
         # cost: arithmetic ops of the task (remat work is small)
