@@ -633,7 +633,7 @@ class _Program:
     def store(self, slot, idx, e):
         self.em.store(int(slot[1]), idx, e)
 
-    def run(self, trees=None, zero_fill=True, cols=None, fext=False, lowmem=False, full_window=False):
+    def run(self, trees=None, zero_fill=True, cols=None, fext=False, lowmem=False, full_window=False, delta=True):
         """Emit the whole one-knot program.  Every op carries a task tag:
         'in' / 'xf' (input loads, joint transforms: re-materialised by each
         consumer), then per root tree t: rnea0.t, ia.t, minv.t.j, fd.t,
@@ -695,8 +695,10 @@ class _Program:
                 em.task = f"rnea1.{t}"
                 if self.lowmem:
                     R = self.emit_rnea(tree, qdd)  # fewer values live across the Minv/FD phase
-                else:
+                elif delta:
                     R = self.emit_rnea_delta(tree, qdd, R0)
+                else:
+                    R = self.emit_rnea(tree, qdd, v_in=(R0["v"], R0["Xv"]))
                 self.emit_xcf(tree, R)
                 for o, kind in (("o0", "q"), ("o1", "qd")):
                     for c in tree:
@@ -818,15 +820,14 @@ TUNED[("chain7", "gradFD", "f64")] = {"park": False, "bk": 32}
 # DRAM 1.64 -> 1.11 GB per launch for 1.06 GB compulsory); fp32 is slower
 # that way (0.56 -> 0.84 ms) and keeps the shared-memory row
 TUNED[("chain7", "gradFD", "f64")].update({"tmem_row": True, "prefetch_dist": 24, "prefetch_slack": 3})
+# the delta form of the second RNEA keeps rnea0's forces live across Minv/FD:
+# fewer ops but more spills in chain7's thread-per-knot kernels (2^20: fp64
+# 1.093 -> 1.120 ms, fp32 0.563 -> 0.606 ms); their warp-specialised kernels keep it
+for _d in DTYPES:
+    TUNED.setdefault(("chain7", "gradFD", _d), {})["thread_delta_rnea"] = False
 # 32-knot CTAs: finer-grained CTA turnover (staging / write-back barriers),
 # measured 1.35 -> 1.22 ms (fp64) and 0.64 -> 0.60 ms (fp32) at N = 2^20
-TUNED[("chain7", "gradFD", "f32")] = {"bk": 32}
-# rollouts (B=128, H=64, gradFD fp64): per-step launches replayed from a graph
-# 0.71 ms vs the fused kernel 0.76 ms (equal at B=4096); quad12 fused 0.32 vs
-# 0.40 ms keeps the default
-for _a in ("FD", "gradFD"):
-    for _d in DTYPES:
-        TUNED.setdefault(("chain7", _a, _d), {})["rollout_fused"] = False
+TUNED.setdefault(("chain7", "gradFD", "f32"), {}).update({"bk": 32})
 # the fine-grained schedule ("fs", fsched.py) measured slower than the task
 # schedule at every small N for chain7 (gradFD fp64 N=128: 10.7 vs 9.9 us;
 # ID: 3.4 vs 2.9 us; profiles/small_n_r2.md), so no robot compiles it by default
@@ -937,12 +938,16 @@ def stage_outputs(model, alg, dtype, bk):
 
 
 def generate_knot(model, alg, dtype, trees=None, zero_fill=True, cols=None, fext=False, lowmem=False,
-                  full_window=False):
+                  full_window=False, delta=None):
     """The one-knot program as an op list (`_Emit`).  trees: restrict to
     these root trees (a 'part'; its outputs are the trees' blocks);
-    zero_fill: also store the structural zeros outside the blocks emitted."""
+    zero_fill: also store the structural zeros outside the blocks emitted;
+    delta: gradFD's second RNEA as a delta from the first (default: tuning
+    "delta_rnea")."""
+    if delta is None:
+        delta = bool(tuning(model, alg, dtype).get("delta_rnea", True))
     return _Program(model, alg, dtype).run(trees, zero_fill, None if cols is None else frozenset(cols), fext,
-                                           lowmem, full_window)
+                                           lowmem, full_window, delta)
 
 
 _FLOPS = {"fma": 2, "mul": 1, "add": 1, "sub": 1, "rcp": 1}
@@ -1715,7 +1720,9 @@ def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=Fal
     tmem > 0: that many of the imports it reloads most are homed in tensor
     memory (tmem_homes) -- the CTA must be 4 warps (one per TMEM lane quadrant)."""
     if em is None:
-        em = generate_knot(model, alg, dt, trees, zero_fill, fext=fext)
+        tk = tuning(model, alg, dt)
+        em = generate_knot(model, alg, dt, trees, zero_fill, fext=fext,
+                           delta=bool(tk.get("thread_delta_rnea", tk.get("delta_rnea", True))))
     L = _layout(model, alg, dt, em, over=over)
     n = L["n"]
     space = "shared" if L["stage"] else "global"
