@@ -18,4 +18,4 @@ kernels.compile_library(models.load('$robot'), algorithms=algs, dtypes=dts)" || 
   else
     RBD_PARTIAL_BUILD=1 RBD_TUNING="$v" timeout 300 python tools/time_kernel.py --robot $robot --alg $alg --dtype $dt --n "$@"
   fi
-done < ${VARIANTS:-tools/variants.txt}
+done < ${VARIANTS:?set VARIANTS to a file of tuning JSON lines (tools/experiments/)}
