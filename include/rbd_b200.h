@@ -58,6 +58,8 @@ enum rbd_dtype { RBD_F32 = 0, RBD_F64 = 1 };
 
 #define RBD_EINVAL (-1)   /* bad algorithm / dtype / NULL pointer / N < 0 */
 #define RBD_ESESSION (-2) /* bad or exhausted session */
+#define RBD_ENONFINITE (-3) /* host-buffer entries: an input holds NaN or Inf (the reference's
+                               refdyn._check_state raises ValueError); outputs are undefined */
 
 typedef struct rbd_info {
   int32_t abi_version;     /* RBD_ABI_VERSION */

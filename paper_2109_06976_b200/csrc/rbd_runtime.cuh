@@ -1121,8 +1121,27 @@ struct rbd_session {
   size_t slot_bytes;
   cudaStream_t stream[RBD_MAX_SLOTS];
   unsigned char* dbuf[RBD_MAX_SLOTS];
-  unsigned char* hstage;  // pinned, RBD_ZC_BYTES
+  unsigned char* hstage;  // pinned, RBD_ZC_BYTES (+ 256: the non-finite input flag)
+  unsigned* dflag;        // device view of that flag (mapped)
 };
+
+// any non-finite element of a[0, count) sets *flag (device input check of the
+// chunked host path; the small-batch path checks on the host)
+template <class T>
+__global__ void rbd_finite_kernel(const T* __restrict__ a, long long count, unsigned* flag) {
+  bool bad = false;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x)
+    bad |= !isfinite(a[i]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
+template <class T>
+static bool rbd_host_finite(const void* p, int64_t count) {
+  const T* a = (const T*)p;
+  for (int64_t i = 0; i < count; ++i)
+    if (!isfinite(a[i])) return false;
+  return true;
+}
 
 // device address of a host pointer when it is page-locked and mapped, else nullptr
 static inline const void* rbd_mapped(const void* p) {
@@ -1156,8 +1175,13 @@ extern "C" int rbd_session_create(int device, int64_t chunk_knots, int32_t slots
   s->chunk = chunk_knots;
   s->slots = slots;
   s->slot_bytes = (size_t)per_knot * (size_t)chunk_knots * sizeof(double) + 10 * 256;
-  e = cudaHostAlloc((void**)&s->hstage, RBD_ZC_BYTES, cudaHostAllocMapped | cudaHostAllocPortable);
+  e = cudaHostAlloc((void**)&s->hstage, RBD_ZC_BYTES + 256, cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e == cudaSuccess) {
+    s->dflag = (unsigned*)rbd_mapped(s->hstage + RBD_ZC_BYTES);
+    if (!s->dflag) e = cudaErrorInvalidValue;
+  }
   if (e != cudaSuccess) {
+    if (s->hstage) cudaFreeHost(s->hstage);
     delete s;
     cudaSetDevice(prev);
     return (int)e;
@@ -1223,6 +1247,14 @@ static int rbd_run_host_impl(rbd_session* s, int alg, int dtype, const void* q, 
   for (int a = 0; a < e->n_inputs; ++a) in_bytes += (size_t)(N * iext[a]) * es;
   for (int b = 0; b < 3; ++b) out_bytes += (size_t)(N * ext[b]) * es;
   if (in_bytes + out_bytes + 8 * 256 <= RBD_ZC_BYTES) {
+    // non-finite inputs are rejected before any work (refdyn._check_state)
+    for (int a = 0; a < e->n_inputs; ++a) {
+      const bool ok = es == 8 ? rbd_host_finite<double>(hin[a], N * iext[a]) : rbd_host_finite<float>(hin[a], N * iext[a]);
+      if (!ok) {
+        cudaSetDevice(prev);
+        return RBD_ENONFINITE;
+      }
+    }
     // small batch: the kernel reads its inputs straight from pinned host
     // memory (the caller's buffers when page-locked, else the pinned stage);
     // outputs go to device memory and come back with ONE copy -- a kernel
@@ -1291,6 +1323,10 @@ static int rbd_run_host_impl(rbd_session* s, int alg, int dtype, const void* q, 
     cudaSetDevice(prev);
     return rc;
   }
+  // non-finite inputs: each chunk's staged inputs are checked on the device
+  // (one pass over bytes already in HBM), the verdict read after the final sync
+  volatile unsigned* hflag = (volatile unsigned*)(s->hstage + RBD_ZC_BYTES);
+  *hflag = 0u;
   for (int64_t c = 0, k0 = 0; k0 < N && rc == 0; ++c, k0 += s->chunk) {
     const int slot = (int)(c % s->slots);
     const int64_t nk = (N - k0) < s->chunk ? (N - k0) : s->chunk;
@@ -1303,6 +1339,12 @@ static int rbd_run_host_impl(rbd_session* s, int alg, int dtype, const void* q, 
       err = cudaMemcpyAsync(p, (const unsigned char*)hin[a] + (size_t)(k0 * iext[a]) * es, bytes,
                             cudaMemcpyHostToDevice, st);
       if (err != cudaSuccess) { rc = (int)err; break; }
+      const long long cnt = (long long)(nk * iext[a]);
+      const unsigned g = (unsigned)((cnt + 255) / 256 < 1184 ? (cnt + 255) / 256 : 1184);
+      if (es == 8)
+        rbd_finite_kernel<double><<<g, 256, 0, st>>>((const double*)p, cnt, s->dflag);
+      else
+        rbd_finite_kernel<float><<<g, 256, 0, st>>>((const float*)p, cnt, s->dflag);
       din[a] = p;
       p += rbd_align256(bytes);
     }
@@ -1325,6 +1367,7 @@ static int rbd_run_host_impl(rbd_session* s, int alg, int dtype, const void* q, 
     err = cudaStreamSynchronize(s->stream[i]);
     if (err != cudaSuccess && rc == 0) rc = (int)err;
   }
+  if (rc == 0 && *hflag) rc = RBD_ENONFINITE;
   cudaSetDevice(prev);
   return rc;
 }

@@ -22,7 +22,9 @@ or a batch `(N, n)`:
 float32 inputs select the fp32 kernels, everything else fp64 (the reference
 precision); `dtype="f32"|"f64"` overrides.  Shapes other than (n,) / (N, n)
 raise ValueError as `refdyn._check_state` does (`refdyn.py:31-38`); host
-inputs containing non-finite values raise ValueError too.  `f_ext` (per-link
+inputs containing non-finite values raise ValueError too (checked by the C
+ABI's host path: on the host for small batches, on the device per staged
+chunk for large ones).  `f_ext` (per-link
 external forces in link coordinates, refdyn.py:79-80) is `(n, 6)` for one
 knot or `(N, n, 6)`, and runs the f_ext kernels (`rbd_<alg>_<dt>_fext`; the
 reference's generated programs have no f_ext input, its refdyn does).
@@ -145,13 +147,8 @@ def _host_fast(model, alg, args):
         single, N = True, 1
     else:
         return None  # the general path raises the reference's error
-    tot = 0.0
-    for x in args:  # one reduction per array; elementwise only if the total is not finite
-        tot += float(np.add.reduce(x, axis=None))
-    if not np.isfinite(tot):
-        for x in args:
-            if not np.all(np.isfinite(x)):
-                raise ValueError("state vector contains non-finite entries")
+    # non-finite inputs: rejected by the host path itself (RBD_ENONFINITE ->
+    # ValueError, refdyn._check_state), checked on the device for big batches
     dt = "f32" if ndt == np.float32 else "f64"
     outs_spec = codegen.outputs(alg, n)
     outs = [_host_empty((N, e), ndt) for _, e in outs_spec]
@@ -209,14 +206,7 @@ def _run(model, alg, args, dtype=None, device=None, f_ext=None, devices=None):
             fx = f_ext.detach().cpu().numpy() if _is_torch(f_ext) else f_ext
             fx = np.ascontiguousarray(np.asarray(fx, dtype=ndt))
             _fext_shape(model, fx, single, N)
-            xs_check = xs + [fx]
-        else:
-            xs_check = xs
-        for x in xs_check:
-            # one reduction pass; the elementwise test only if the sum is not
-            # finite (a non-finite entry, or an overflow of finite ones)
-            if not np.isfinite(np.add.reduce(x, axis=None)) and not np.all(np.isfinite(x)):
-                raise ValueError("state vector contains non-finite entries")
+        # non-finite inputs raise ValueError from the host path (RBD_ENONFINITE)
         outs = [_host_empty((N, e), ndt) for _, e in codegen.outputs(alg, n)]
         runtime.run_host(lib, alg, dt, xs, outs, N, device=device, f_ext=fx, devices=devices)
     shaped = []

@@ -28,6 +28,8 @@ class LaunchError(RuntimeError):
 def check(rc, what):
     if rc == 0:
         return
+    if rc == -3:  # RBD_ENONFINITE (refdyn._check_state)
+        raise ValueError("state vector contains non-finite entries")
     if rc < 0:
         raise ValueError(f"{what}: invalid argument (rbd error {rc})")
     name = _CUDA_ERRORS.get(rc, "cudaError")

@@ -180,6 +180,31 @@ def test_errors_like_reference():
         dynamics.rnea(m, np.zeros(7), np.zeros(7), np.zeros(7), f_ext=np.full((7, 6), np.nan))
 
 
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_nonfinite_inputs_rejected_on_device(dt):
+    """Large host batches are checked on the device, chunk by chunk: one NaN
+    deep in a later chunk raises ValueError (refdyn._check_state), and the
+    session's flag is re-armed for the next call."""
+    m = models.load("chain7")
+    ndt = np.float64 if dt == "f64" else np.float32
+    rng = np.random.default_rng(4)
+    N = 300_000  # several pipeline chunks
+    q, qd, tau = (rng.uniform(-1, 1, (N, 7)).astype(ndt) for _ in range(3))
+    bad = qd.copy()
+    bad[N - 17, 3] = np.nan
+    with pytest.raises(ValueError):
+        dynamics.forward_dynamics(m, q, bad, tau)
+    bad = tau.copy()
+    bad[123_456, 0] = np.inf
+    with pytest.raises(ValueError):
+        dynamics.fd_grad(m, q, qd, bad)
+    qdd = dynamics.forward_dynamics(m, q[:64], qd[:64], tau[:64])
+    ref = R.evaluate_batch(m, "FD", *(x[:64].astype(np.float64) for x in (q, qd, tau)))["qdd_out"]
+    assert rel_err(qdd, ref) < TOL[dt]
+    qdd = dynamics.forward_dynamics(m, q, qd, tau)  # flag re-armed after the failures
+    assert np.all(np.isfinite(qdd))
+
+
 @pytest.mark.parametrize("name", MODELS)
 @pytest.mark.parametrize("dt", ["f64", "f32"])
 def test_fext_matches_reference(name, dt):
