@@ -1280,7 +1280,7 @@ def row_homes(em, scratch_base):
 
 
 def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None, plan=None, tslot=None,
-             trow=False, row_base=0):
+             trow=False, row_base=0, dense=None):
     """Device backend: the op list as PTX for one inline-asm block.
 
     Operand %0 is the 32-bit shared address of the knot's input row (inputs,
@@ -1483,6 +1483,9 @@ def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None
             if plan is not None and plan.park:
                 if not isinstance(op[3], float):  # constants come from the output map
                     lines.append(f"st.shared.{t} [%0+{plan.outslot[(op[1], op[2])] * es}], {use(op[3])};")
+            elif dense is not None:  # a part's outputs, staged densely (element map write-back)
+                v = creg(op[3]) if isinstance(op[3], float) else use(op[3])
+                lines.append(f"st.shared.{t} [%1+{dense[(op[1], op[2])] * es}], {v};")
             else:
                 v = creg(op[3]) if isinstance(op[3], float) else use(op[3])
                 lines.append(f"{pred}st.{out_space}.{t} [%{1 + op[1]}+{op[2] * es}], {v};")
@@ -1575,9 +1578,21 @@ def _layout(model, alg, dt, em, device=True, over=None):
         smem = bk * max(row, sout) * es
         # a row longer than a TMEM lane (e.g. the f_ext program), or outputs
         # that do not fit the staging of 2 CTAs, keep the shared-memory row
+        # a part program (a subset of the root trees) stages only the elements
+        # it stores, densely, and writes them back through an element map
+        stored = sorted({(op[1], op[2]) for op in em.ops if op[0] == "st"})
+        tpart = None
+        if len(stored) < sum(ext):
+            offs = [0, ext[0], ext[0] + ext[1]]
+            tpart = [offs[k] + idx for k, idx in stored]
+            sout_t = _odd(len(stored))
+        else:
+            sout_t = sout
+        smem = bk * max(row, sout_t) * es
         if plan.nslots * tw <= tcols_thread and 2 * (smem + CTA_SMEM_RESERVED) <= SM_SMEM:
-            return dict(n=n, ext=ext, nin=nin, nsc=nsc, bk=bk, stage=True, sin=row, sout=sout, plan=plan, minb=2,
-                        park=False, lo=em.lo, np=em.np, in_layout=em.in_layout, trow=True, tcols=tcols_thread)
+            return dict(n=n, ext=ext, nin=nin, nsc=nsc, bk=bk, stage=True, sin=row, sout=sout_t, plan=plan, minb=2,
+                        park=False, lo=em.lo, np=em.np, in_layout=em.in_layout, trow=True, tcols=tcols_thread,
+                        tpart=tpart, dense={kv: j for j, kv in enumerate(stored)} if tpart else None)
         plan = None
     if tn.get("ra") and device:
         homes = row_homes(em, em.in_total)
@@ -1644,6 +1659,8 @@ def _struct_head(model, alg, dt, L, fl, name=None):
         f"  static constexpr int TCOLS = {L.get('tcols', 0)};  // TMEM columns per CTA (split-column imports / row)",
         f"  static constexpr bool TROW = {'true' if L.get('trow') else 'false'};  // the row lives in TMEM; "
         "outputs staged over the input staging",
+        f"  static constexpr bool TPART = {'true' if L.get('tpart') else 'false'};  // ... densely, a part's "
+        "elements only",
     ]
 
 
@@ -1738,7 +1755,7 @@ def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=Fal
                                   "quadrants)")
         L["tcols"] = tmem_alloc(tc, L["bk"]) if tslot else 0
     body, sc = ptx_body(em, em.in_total, space, tn["sync_every"], tn["reload_dist"], ctab, plan, tslot=tslot,
-                        trow=bool(L.get("trow")), row_base=L["sin"] if L.get("trow") else 0)
+                        trow=bool(L.get("trow")), row_base=L["sin"] if L.get("trow") else 0, dense=L.get("dense"))
     ra = (f"// register budget: {plan.reloads} reloads, {plan.stores} parked values, row {L['sin']} slots, "
           f"{L['minb']} CTAs of {L['bk']} per SM" if plan is not None else "// ptxas register allocation")
     src = [
@@ -1751,6 +1768,13 @@ def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=Fal
         + _struct_head(model, alg, dt, L, em.flops, name) + [
         f"  static constexpr int NX = {nx};  // values exported per knot to the split scratch",
     ]
+    if L.get("tpart"):
+        nm = name or f"Knot_{alg}_{dt}"
+        src.insert(src.index("#pragma once") + 2,
+                   f"__constant__ unsigned short rbd_te_{nm}[{len(L['tpart'])}] = "
+                   f"{{{', '.join(str(e) for e in L['tpart'])}}};")
+        src.append(f"  static constexpr int NOUT = {len(L['tpart'])};  // output elements this part writes")
+        src.append(f"  __device__ __forceinline__ static const unsigned short* oelem() {{ return rbd_te_{nm}; }}")
     if L.get("park"):
         nm = name or f"Knot_{alg}_{dt}"
         src.append(f"  static constexpr int NOUT = {L['nout']};  // output elements this program writes")

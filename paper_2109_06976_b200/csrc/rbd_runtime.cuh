@@ -244,11 +244,28 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
     T* o = s_out + tid * K::SOUT;
     K::run_dev(my, o, o + K::E0, o + K::E0 + K::E1, 1u, xb, tm);
     __syncthreads();
-    // coalesced write-back, one output array at a time
-    auto staged = [&](int off) { return [=](int k, int e) { return s_out[k * K::SOUT + off + e]; }; };
-    rbd_write_back<T, K::E0, BK>(o0 + base * K::E0, nk, tid, staged(0));
-    if constexpr (K::E1 > 0) rbd_write_back<T, K::E1, BK>(o1 + base * K::E1, nk, tid, staged(K::E0));
-    if constexpr (K::E2 > 0) rbd_write_back<T, K::E2, BK>(o2 + base * K::E2, nk, tid, staged(K::E0 + K::E1));
+    if constexpr (K::TPART) {
+      // a part program's elements, staged densely: element map write-back
+      constexpr int M = K::NOUT;
+      const unsigned short* oe = K::oelem();
+      for (int idx = tid; idx < nk * M; idx += BK) {
+        const int k = idx / M, j = idx - k * M;
+        const int e = oe[j];
+        const T v = s_out[k * K::SOUT + j];
+        if (e < K::E0)
+          __stcs(o0 + (base + k) * K::E0 + e, v);
+        else if (e < K::E0 + K::E1)
+          __stcs(o1 + (base + k) * K::E1 + (e - K::E0), v);
+        else
+          __stcs(o2 + (base + k) * K::E2 + (e - K::E0 - K::E1), v);
+      }
+    } else {
+      // coalesced write-back, one output array at a time
+      auto staged = [&](int off) { return [=](int k, int e) { return s_out[k * K::SOUT + off + e]; }; };
+      rbd_write_back<T, K::E0, BK>(o0 + base * K::E0, nk, tid, staged(0));
+      if constexpr (K::E1 > 0) rbd_write_back<T, K::E1, BK>(o1 + base * K::E1, nk, tid, staged(K::E0));
+      if constexpr (K::E2 > 0) rbd_write_back<T, K::E2, BK>(o2 + base * K::E2, nk, tid, staged(K::E0 + K::E1));
+    }
   } else {
     // every thread runs the program (CTA barriers inside); stores of the
     // padding threads of the last CTA are predicated off

@@ -202,6 +202,40 @@ def test_ws_split_programs(name, alg):
         assert rel_err(got[None], g[f"{alg}.{nm}"][2:3]) < 1e-12, (name, alg, nm)
 
 
+@pytest.mark.parametrize("name,trees", [("humanoid30", (1,)), ("humanoid30", (2,)), ("quad12", (3,))])
+def test_part_program_with_tmem_row(name, trees):
+    """A part program (one root tree of several) with its row in TMEM and its
+    outputs staged densely: every element it stores lands at its dense slot,
+    and the element map puts it back where the reference has it."""
+    g = golden(name)
+    m = models.load(name)
+    n = m.n_dof
+    em = codegen.generate_knot(m, "gradFD", "f64", trees=trees, zero_fill=False)
+    L = codegen._layout(m, "gradFD", "f64", em, over={"tmem_row": True})
+    assert L.get("trow") and L.get("tpart"), "the part should take the TMEM-row layout"
+    ctab = codegen.ConstTable("K", "f64")
+    lines, sc = codegen.ptx_body(em, em.in_total, "shared", ctab=ctab, plan=L["plan"], trow=True,
+                                 row_base=L["sin"], dense=L["dense"])
+    k = 2
+    x_full = _inputs(g, "gradFD", k, n)
+    lo, np_ = em.lo, em.np
+    x = np.concatenate([x_full[a * n + lo:a * n + lo + np_] for a in range(3)])
+    row = {i: float(v) for i, v in enumerate(x)}
+    for j, slot in enumerate(sc):
+        row[em.in_total + 2 * j] = math.sin(x[slot])
+        row[em.in_total + 2 * j + 1] = math.cos(x[slot])
+    staged = {}
+    ptxsim.run_block(lines, [row, staged, {}, {}, None, None, {}], [8, 8, 8, 8, 8, 8, 1],
+                     consts={"K": sorted(ctab.index, key=ctab.index.get)})
+    assert len(staged) == len(L["tpart"])
+    ext = [e for _, e in codegen.outputs("gradFD", n)]
+    ref = np.concatenate([g[f"gradFD.{nm}"][k] for nm, _ in codegen.outputs("gradFD", n)])
+    got = np.array([staged[j] for j in range(len(L["tpart"]))])
+    want = ref[np.array(L["tpart"])]
+    assert np.max(np.abs(got - want)) <= 1e-12 * max(1.0, np.max(np.abs(ref))), (name, trees)
+    assert sum(ext) > len(L["tpart"])
+
+
 def test_ws_schedule_properties():
     m = models.load("humanoid30")
     P = wsched.plan(m, "gradFD", "f64", 16)
