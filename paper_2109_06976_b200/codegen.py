@@ -809,6 +809,10 @@ TUNING_DEFAULT = {
     "wsplit_groups": 6,  # wsplit: column groups of the big tree (CTA-row variants of kernel B)
     "wsplit_warps": 16,  # wsplit: warps of the prefix kernel A
     "wsplit_max_n": 0,   # wsplit: batch size up to which the split small-batch path runs
+    "bulk_out": False,   # thread + tmem_row: outputs staged array-major in shared memory and written
+                         # back with TMA bulk stores (cp.async.bulk.global.shared::cta), one per array
+    "l2_prefetch": 0,    # thread: each CTA bulk-prefetches (TMA) the input slabs of the CTA this many
+                         # waves (148 SMs x MINB CTAs) ahead into L2 (0: off)
 }
 TUNED = {}
 # measured on B200 (N = 2^20): chain7 gradFD fp64 is compute-bound at 6 warps/SM
@@ -848,6 +852,16 @@ for _a in ALGORITHMS:
             # fp32 5.1 -> 3.3 us (and slower than one CTA from N=1024)
             TUNED[("quad12", _a, _d)].update({"maps": ["thread", "ws", "wc"], "wc_warps": 16, "wc_variants": 8,
                                               "wc_max_n": 256})
+        # thread-per-knot kernel: each CTA bulk-prefetches (TMA) the input slabs
+        # of the CTA one wave ahead into L2: 2^20 knots gradFD fp64 557 -> 551
+        # us, fp32 344 -> 341, FD fp32 91.5 -> 89.0 (tools/experiments)
+        TUNED[("quad12", _a, _d)]["l2_prefetch"] = 1
+        if _d == "f64" and _a in ("gradFD", "gradID", "Minv"):
+            # the knot's row in tensor memory (8 warps x 255 registers), the
+            # structural zeros (cross-leg blocks) not staged but supplied by
+            # the write-back's element map: gradFD 2^20 550 -> 444 us, gradID
+            # 436 -> 422, Minv 205 -> 199 (FD / ID and fp32: slower that way)
+            TUNED[("quad12", _a, _d)].update({"tmem_row": True, "trow_zmap": True})
         # humanoid30: small batches on the warp-specialised kernel; large ones
         # per root tree (torso tree, two legs)
         TUNED[("humanoid30", _a, _d)] = {"maps": ["ws"], "warps": 16, "minb": 1, "parts": [[0], [1], [2]],
@@ -1483,7 +1497,9 @@ def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None
             if plan is not None and plan.park:
                 if not isinstance(op[3], float):  # constants come from the output map
                     lines.append(f"st.shared.{t} [%0+{plan.outslot[(op[1], op[2])] * es}], {use(op[3])};")
-            elif dense is not None:  # a part's outputs, staged densely (element map write-back)
+            elif dense is not None:  # staged densely (element map write-back)
+                if (op[1], op[2]) not in dense:
+                    continue  # a structural zero: the write-back map supplies it
                 v = creg(op[3]) if isinstance(op[3], float) else use(op[3])
                 lines.append(f"st.shared.{t} [%1+{dense[(op[1], op[2])] * es}], {v};")
             else:
@@ -1562,9 +1578,14 @@ def _layout(model, alg, dt, em, device=True, over=None):
         # 2 per SM (8 warps, 255 registers), each CTA 256 columns; shared
         # memory only stages the inputs and then, aliased over them, the
         # outputs in element order for the coalesced write-back
-        bk = 128
-        tcols_thread = 256
-        budget = (255 - REG_OVERHEAD) // (2 if dt == "f64" else 1)
+        tbk = int(tn.get("trow_bk", 128))  # 256: one 8-warp CTA per SM (all warps on one TMEM allocation)
+        # CTAs per SM: 2 (255 registers, 256 TMEM columns per thread); 3-4
+        # with per-thread global output stores (no output staging; 170 / 128
+        # registers, 128 columns)
+        tstage = bool(tn.get("trow_stage", True))
+        ctas_sm = int(tn.get("trow_ctas", 256 // tbk))
+        tcols_thread = 1 << ((512 // (ctas_sm * (tbk // 128))).bit_length() - 1)
+        budget = (min(255, 65536 // (ctas_sm * tbk)) - REG_OVERHEAD) // (2 if dt == "f64" else 1)
         if tn.get("ra_budget"):
             budget = min(budget, int(tn["ra_budget"]))
         pf = None
@@ -1575,24 +1596,39 @@ def _layout(model, alg, dt, em, device=True, over=None):
         plan = SpillPlan(em, budget, homes, base, park_outputs=False, prefetch=pf)
         tw = 2 if es == 8 else 1
         row = _odd(base)
-        smem = bk * max(row, sout) * es
+        smem = tbk * max(row, sout) * es
         # a row longer than a TMEM lane (e.g. the f_ext program), or outputs
         # that do not fit the staging of 2 CTAs, keep the shared-memory row
         # a part program (a subset of the root trees) stages only the elements
         # it stores, densely, and writes them back through an element map
         stored = sorted({(op[1], op[2]) for op in em.ops if op[0] == "st"})
-        tpart = None
+        offs = [0, ext[0], ext[0] + ext[1]]
+        tpart = zmap = dense = None
         if len(stored) < sum(ext):
-            offs = [0, ext[0], ext[0] + ext[1]]
             tpart = [offs[k] + idx for k, idx in stored]
+            dense = {kv: j for j, kv in enumerate(stored)}
             sout_t = _odd(len(stored))
         else:
             sout_t = sout
-        smem = bk * max(row, sout_t) * es
-        if plan.nslots * tw <= tcols_thread and 2 * (smem + CTA_SMEM_RESERVED) <= SM_SMEM:
-            return dict(n=n, ext=ext, nin=nin, nsc=nsc, bk=bk, stage=True, sin=row, sout=sout_t, plan=plan, minb=2,
-                        park=False, lo=em.lo, np=em.np, in_layout=em.in_layout, trow=True, tcols=tcols_thread,
-                        tpart=tpart, dense={kv: j for j, kv in enumerate(stored)} if tpart else None)
+            nonzero = sorted({(op[1], op[2]) for op in em.ops
+                              if op[0] == "st" and not (isinstance(op[3], float) and op[3] == 0.0)})
+            if tn.get("trow_zmap") and len(nonzero) < sum(ext):
+                # structural zeros (e.g. cross-leg blocks) are not staged:
+                # the write-back takes element e from dense slot zmap[e], or 0
+                dense = {kv: j for j, kv in enumerate(nonzero)}
+                zmap = [-1] * sum(ext)
+                for (k, idx), j in dense.items():
+                    zmap[offs[k] + idx] = j
+                sout_t = _odd(len(nonzero))
+        if not tstage:
+            sout_t, tpart, zmap, dense = 0, None, None, None
+        smem = tbk * max(row, sout_t) * es + (2 * len(zmap) if zmap else 0)
+        if plan.nslots * tw <= tcols_thread and ctas_sm * (smem + CTA_SMEM_RESERVED) <= SM_SMEM:
+            return dict(n=n, ext=ext, nin=nin, nsc=nsc, bk=tbk, stage=tstage, sin=row, sout=sout_t, plan=plan,
+                        minb=ctas_sm, park=False, lo=em.lo, np=em.np, in_layout=em.in_layout, trow=True,
+                        tcols=tmem_alloc(tcols_thread, tbk),
+                        bulk=bool(tstage and tpart is None and zmap is None and tn.get("bulk_out")),
+                        tpart=tpart, zmap=zmap, dense=dense)
         plan = None
     if tn.get("ra") and device:
         homes = row_homes(em, em.in_total)
@@ -1661,6 +1697,10 @@ def _struct_head(model, alg, dt, L, fl, name=None):
         "outputs staged over the input staging",
         f"  static constexpr bool TPART = {'true' if L.get('tpart') else 'false'};  // ... densely, a part's "
         "elements only",
+        f"  static constexpr int L2PF = {int(tuning(model, alg, dt).get('l2_prefetch', 0))};  // input slabs "
+        "bulk-prefetched into L2 this many CTA waves ahead (0: off)",
+        f"  static constexpr bool BULK = {'true' if L.get('bulk') else 'false'};  // outputs staged array-major, "
+        "written back by TMA bulk stores",
     ]
 
 
@@ -1775,6 +1815,13 @@ def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=Fal
                    f"{{{', '.join(str(e) for e in L['tpart'])}}};")
         src.append(f"  static constexpr int NOUT = {len(L['tpart'])};  // output elements this part writes")
         src.append(f"  __device__ __forceinline__ static const unsigned short* oelem() {{ return rbd_te_{nm}; }}")
+    if L.get("zmap"):
+        nm = name or f"Knot_{alg}_{dt}"
+        src.insert(src.index("#pragma once") + 2,
+                   f"__constant__ short rbd_zm_{nm}[{len(L['zmap'])}] = "
+                   f"{{{', '.join(str(e) for e in L['zmap'])}}};")
+        src.append(f"  static constexpr int NZM = {len(L['zmap'])};  // output elements: dense staging slot or -1 (0)")
+        src.append(f"  __device__ __forceinline__ static const short* zmap() {{ return rbd_zm_{nm}; }}")
     if L.get("park"):
         nm = name or f"Knot_{alg}_{dt}"
         src.append(f"  static constexpr int NOUT = {L['nout']};  // output elements this program writes")

@@ -97,6 +97,84 @@ __host__ __device__ constexpr int rbd_max_inw() {
 
 template <class K>
 __host__ __device__ constexpr bool rbd_ofull() { return rbd_park_traits<K>::ofull; }
+template <class K, class = void>
+struct rbd_l2pf_traits {
+  static constexpr int waves = 0;
+};
+template <class K>
+struct rbd_l2pf_traits<K, decltype((void)K::L2PF, void())> {
+  static constexpr int waves = K::L2PF;
+};
+
+template <class K, class = void>
+struct rbd_zmap_traits {
+  static constexpr int n = 0;
+};
+template <class K>
+struct rbd_zmap_traits<K, decltype((void)K::NZM, void())> {
+  static constexpr int n = K::NZM;
+};
+template <class K>
+__host__ __device__ constexpr int rbd_nzm() { return rbd_zmap_traits<K>::n; }
+
+template <class K, class = void>
+struct rbd_bulk_traits {
+  static constexpr bool on = false;
+};
+template <class K>
+struct rbd_bulk_traits<K, decltype((void)K::BULK, void())> {
+  static constexpr bool on = K::BULK;
+};
+
+// TMA bulk store of one output array's CTA range: src = [nk][E] staged
+// array-major in shared memory, dst = the knots' contiguous global rows.
+// One elected thread issues it (bulk-group completion); the caller waits for
+// the shared-memory reads before the staging is reused or the CTA exits.
+// Falls back to a cooperative 16-byte copy when the range is not a whole
+// number of 16-byte units or dst is not 16-byte aligned (bulk-copy rule).
+template <class T, int E, int NT>
+__device__ __forceinline__ bool rbd_bulk_store(T* dst, const T* src, int nk, int tid) {
+  const unsigned bytes = (unsigned)(nk * E * (int)sizeof(T));
+  const bool ok = (bytes % 16 == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+  if (ok) {
+    if (tid == 0)
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                   "r"((unsigned)__cvta_generic_to_shared(src)), "r"(bytes)
+                   : "memory");
+  } else {
+    for (int i = tid; i < nk * E; i += NT) __stcs(dst + i, src[i]);
+  }
+  return ok;
+}
+
+#define RBD_SMS 148  // B200
+// TMA bulk prefetch into L2 of the input slabs of the CTA `waves` waves
+// ahead (the one that will take this SM slot): its input loads then hit L2
+// instead of waiting on HBM behind the output write stream.  One thread per
+// input array; the slab is [BK knots][ins(a)] contiguous (a part program's
+// window is inside it); the 16-byte-aligned body only (bulk-copy rule).
+template <class K>
+__device__ __forceinline__ void rbd_prefetch_slabs(const void* q, const void* qd, const void* u, const void* fx,
+                                                   long long N, int tid) {
+  constexpr int waves = rbd_l2pf_traits<K>::waves;
+  if constexpr (waves > 0) {
+    typedef typename K::T T;
+    if (tid < K::NIN) {
+      const long long nb = (long long)blockIdx.x + (long long)waves * RBD_SMS * K::MINB;
+      const long long k0 = nb * K::BK;
+      if (k0 < N) {
+        const long long nk = N - k0 < K::BK ? N - k0 : K::BK;
+        const void* arr = tid == 0 ? q : (tid == 1 ? qd : (tid == 2 ? u : fx));
+        const char* lo = reinterpret_cast<const char*>(arr) + k0 * K::ins(tid) * (long long)sizeof(T);
+        const char* hi = lo + nk * K::ins(tid) * (long long)sizeof(T);
+        const char* a = reinterpret_cast<const char*>((reinterpret_cast<uintptr_t>(lo) + 15) & ~(uintptr_t)15);
+        const unsigned bytes = (unsigned)((hi - a) & ~15LL);
+        if (hi > a && bytes)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
+      }
+    }
+  }
+}
 
 // coalesced write-back of nk knots x E elements of one output array, 16-byte
 // streaming stores when E is a multiple of the vector width and dst is
@@ -151,6 +229,7 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
   const long long left = N - base;
   const int nk = left < BK ? (int)left : BK;
   const int tid = threadIdx.x;
+  rbd_prefetch_slabs<K>(q, qd, u, fx, N, tid);
 
   // all input loads of this thread are issued before the first smem store
   // (one HBM round trip per CTA, not one per element); input a contributes
@@ -184,6 +263,11 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
       s_map[j] = K::omap()[j];
       if constexpr (!rbd_ofull<K>()) s_elem[j] = K::oelem()[j];
     }
+  }
+  // TMEM row with structural zeros unstaged: element -> dense staging slot (or -1)
+  short* s_zm = reinterpret_cast<short*>(s_in + BK * (K::SIN > K::SOUT ? K::SIN : K::SOUT));
+  if constexpr (rbd_nzm<K>() > 0) {
+    for (int j = tid; j < rbd_nzm<K>(); j += BK) s_zm[j] = K::zmap()[j];
   }
   __syncthreads();
   // tensor memory for the imports a split column kernel homes there: one
@@ -240,6 +324,21 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
       if constexpr (K::E2 > 0)
         rbd_write_back<T, K::E2, BK>(o2 + base * K::E2, nk, tid, from_map(K::E0 + K::E1));
     }
+  } else if constexpr (rbd_bulk_traits<K>::on) {
+    // array-major staging [BK][E0] | [BK][E1] | [BK][E2]: each array's CTA
+    // range is one contiguous block in shared and in global memory
+    T* so1 = s_out + BK * K::E0;
+    T* so2 = so1 + BK * K::E1;
+    K::run_dev(my, s_out + tid * K::E0, so1 + tid * K::E1, so2 + tid * K::E2, 1u, xb, tm);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy stores -> TMA reads
+    __syncthreads();
+    rbd_bulk_store<T, K::E0, BK>(o0 + base * K::E0, s_out, nk, tid);
+    if constexpr (K::E1 > 0) rbd_bulk_store<T, K::E1, BK>(o1 + base * K::E1, so1, nk, tid);
+    if constexpr (K::E2 > 0) rbd_bulk_store<T, K::E2, BK>(o2 + base * K::E2, so2, nk, tid);
+    if (tid == 0) {
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging read before the CTA exits
+    }
   } else if constexpr (K::STAGE) {
     T* o = s_out + tid * K::SOUT;
     K::run_dev(my, o, o + K::E0, o + K::E0 + K::E1, 1u, xb, tm);
@@ -259,6 +358,16 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
         else
           __stcs(o2 + (base + k) * K::E2 + (e - K::E0 - K::E1), v);
       }
+    } else if constexpr (rbd_nzm<K>() > 0) {
+      auto zm = [&](int off) {
+        return [=](int k, int e) {
+          const int j = s_zm[off + e];
+          return j >= 0 ? s_out[k * K::SOUT + j] : T(0);
+        };
+      };
+      rbd_write_back<T, K::E0, BK>(o0 + base * K::E0, nk, tid, zm(0));
+      if constexpr (K::E1 > 0) rbd_write_back<T, K::E1, BK>(o1 + base * K::E1, nk, tid, zm(K::E0));
+      if constexpr (K::E2 > 0) rbd_write_back<T, K::E2, BK>(o2 + base * K::E2, nk, tid, zm(K::E0 + K::E1));
     } else {
       // coalesced write-back, one output array at a time
       auto staged = [&](int off) { return [=](int k, int e) { return s_out[k * K::SOUT + off + e]; }; };
@@ -728,8 +837,9 @@ constexpr size_t rbd_smem_bytes() {
   else if constexpr (K::MAP == 1)
     return sizeof(typename K::T) * (size_t)RBD_WS_LANES *
            (K::SIN + (K::ARENA_SMEM ? K::NA : 0) + (K::STAGE ? K::SOUT : 0));
-  else if constexpr (K::TROW)  // input staging and output staging aliased
-    return sizeof(typename K::T) * (size_t)K::BK * (K::SIN > K::SOUT ? K::SIN : K::SOUT);
+  else if constexpr (K::TROW)  // input staging and output staging aliased (+ the zero map)
+    return sizeof(typename K::T) * (size_t)K::BK * (K::SIN > K::SOUT ? K::SIN : K::SOUT) +
+           sizeof(short) * (size_t)rbd_nzm<K>();
   else
     return sizeof(typename K::T) * (size_t)K::BK * (K::SIN + (K::STAGE ? K::SOUT : 0)) +
            sizeof(short) * (size_t)rbd_nout<K>() * (rbd_ofull<K>() ? 1 : 2);
