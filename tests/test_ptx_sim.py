@@ -236,6 +236,42 @@ def test_part_program_with_tmem_row(name, trees):
     assert sum(ext) > len(L["tpart"])
 
 
+@pytest.mark.parametrize("alg", ["gradFD", "gradID", "Minv"])
+def test_tmem_row_zero_map(alg):
+    """quad12's whole program on the TMEM row with its structural zeros not
+    staged (trow_zmap): the program stages only the non-zero outputs, and the
+    write-back's element map (dense slot or -1 = 0) rebuilds every output
+    element the reference has, cross-leg zeros included."""
+    name = "quad12"
+    g = golden(name)
+    m = models.load(name)
+    n = m.n_dof
+    em = codegen.generate_knot(m, alg, "f64")
+    L = codegen._layout(m, alg, "f64", em, over={"tmem_row": True, "trow_zmap": True})
+    assert L.get("trow") and L.get("zmap") and not L.get("tpart")
+    zmap = L["zmap"]
+    ext = [e for _, e in codegen.outputs(alg, n)]
+    assert len(zmap) == sum(ext) and 0 < sum(j >= 0 for j in zmap) < len(zmap)
+    ctab = codegen.ConstTable("K", "f64")
+    lines, sc = codegen.ptx_body(em, em.in_total, "shared", ctab=ctab, plan=L["plan"], trow=True,
+                                 row_base=L["sin"], dense=L["dense"])
+    k = 1
+    x = _inputs(g, alg, k, n)
+    row = {i: 0.0 for i in range(L["sin"])}  # the odd-stride pad slot is copied too
+    row.update({i: float(v) for i, v in enumerate(x)})
+    for j, slot in enumerate(sc):
+        row[em.in_total + 2 * j] = math.sin(x[slot])
+        row[em.in_total + 2 * j + 1] = math.cos(x[slot])
+    staged = {}
+    ptxsim.run_block(lines, [row, staged, {}, {}, None, None, {}], [8, 8, 8, 8, 8, 8, 1],
+                     consts={"K": sorted(ctab.index, key=ctab.index.get)})
+    assert sorted(staged) == sorted(j for j in zmap if j >= 0)
+    got = np.array([staged[j] if j >= 0 else 0.0 for j in zmap])
+    ref = np.concatenate([g[f"{alg}.{nm}"][k].ravel() for nm, _ in codegen.outputs(alg, n)])
+    assert np.max(np.abs(got - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref))), alg
+    assert np.all(ref[np.array(zmap) < 0] == 0.0)
+
+
 def test_ws_schedule_properties():
     m = models.load("humanoid30")
     P = wsched.plan(m, "gradFD", "f64", 16)

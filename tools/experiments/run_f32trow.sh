@@ -1,0 +1,15 @@
+d=gpurun_out
+for r in quad12 chain7; do
+keys=()
+while read -r v; do
+  key=x$(printf '%s' "$v" | md5sum | cut -c1-7); keys+=($key)
+  RBD_PARTIAL_BUILD=1 RBD_TUNING="$v" RBD_BUILD_KEY=$key python tools/experiments/dump_outputs.py $r gradFD f32 $d/o_${key}_$r.npz 65541 2>&1 | tail -1
+done < tools/experiments/variants_f32trow.txt
+for k in ${keys[@]:1}; do python tools/experiments/cmp_outputs.py $d/o_${keys[0]}_$r.npz $d/o_${k}_$r.npz; done | grep -c DIFFER
+rm -f $d/o_*.npz
+VARIANTS=tools/experiments/variants_f32trow.txt bash tools/variants.sh time $r gradFD f32 1048576 2>&1 | python -c "
+import sys, json
+for l in sys.stdin:
+    if l.startswith('{'):
+        d = json.loads(l); print(d['robot'], d['alg'], d['dtype'], d['tuning'], d['N'], round(d['us'], 1))"
+done
