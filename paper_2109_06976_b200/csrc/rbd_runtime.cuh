@@ -55,6 +55,68 @@ RBD_HD void rbd_sincos(float x, float* s, float* c) {
 #endif
 }
 
+// sin and cos of N angles evaluated side by side (fp64): Cody-Waite
+// reduction by pi/2 in two parts, then the classic minimax kernels on
+// [-pi/4, pi/4] (the fdlibm __kernel_sin / __kernel_cos coefficients) and a
+// quadrant select.  N independent chains share each coefficient (one uniform
+// register pair per coefficient, not one per call) and give the scheduler
+// N-way ILP; ~1-2 ulp, well inside the 1e-9 parity bound.  Angles beyond
+// |x| > 2^20 (where the 2-part reduction loses bits) take sincos().
+#if defined(__CUDACC__)
+// out-of-line fallback, so the rarely taken path adds a call, not N inlined
+// copies of libdevice's reduction, to the straight-line kernel body
+static __device__ __noinline__ double2 rbd_sincos_slow(double x) {
+  double2 v;
+  sincos(x, &v.x, &v.y);
+  return v;
+}
+#endif
+
+template <int N>
+RBD_HD void rbd_sincos_batch(const double* x, double* s, double* c) {
+#if defined(__CUDA_ARCH__)
+  // pi/2 = P1 + P2 + O(1e-33); with FMA, x - k P1 is rounded once
+  const double TWO_OVER_PI = 6.366197723675814e-01;
+  const double P1 = 1.5707963267948966e+00, P2 = 6.123233995736766e-17;
+  const double S1 = -1.66666666666666324348e-01, S2 = 8.33333333332248946124e-03,
+               S3 = -1.98412698298579493134e-04, S4 = 2.75573137070700676789e-06,
+               S5 = -2.50507602534068634195e-08, S6 = 1.58969099521155010221e-10;
+  const double C1 = 4.16666666666666019037e-02, C2 = -1.38888888888741095749e-03,
+               C3 = 2.48015872894767294178e-05, C4 = -2.75573143513906633035e-07,
+               C5 = 2.08757232129817482790e-09, C6 = -1.13596475577881948265e-11;
+  bool big = false;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const double k = rint(x[j] * TWO_OVER_PI);
+    const double r = fma(-k, P2, fma(-k, P1, x[j]));
+    const double z = r * r;
+    const double ps = fma(z, fma(z, fma(z, fma(z, fma(z, S6, S5), S4), S3), S2), S1);
+    const double sn = fma(r * z, ps, r);
+    const double pc = fma(z, fma(z, fma(z, fma(z, fma(z, C6, C5), C4), C3), C2), C1);
+    const double cs = fma(z * z, pc, fma(-0.5, z, 1.0));
+    const int q = (int)(long long)k & 3;
+    const double a = (q & 1) ? cs : sn, b = (q & 1) ? sn : cs;
+    s[j] = (q & 2) ? -a : a;
+    c[j] = ((q + 1) & 2) ? -b : b;
+    big |= fabs(x[j]) > 1048576.0;
+  }
+  if (big) {
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+      if (fabs(x[j]) > 1048576.0) {
+        const double2 v = rbd_sincos_slow(x[j]);
+        s[j] = v.x;
+        c[j] = v.y;
+      }
+  }
+#else
+  for (int j = 0; j < N; ++j) {
+    s[j] = sin(x[j]);
+    c[j] = cos(x[j]);
+  }
+#endif
+}
+
 RBD_HD double rbd_fma(double a, double b, double c) { return fma(a, b, c); }
 RBD_HD float rbd_fma(float a, float b, float c) { return fmaf(a, b, c); }
 
