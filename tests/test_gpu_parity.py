@@ -328,3 +328,24 @@ def test_host_path_zero_copy_and_chunked(pinned):
         for (nm, _), o in zip(codegen.outputs("gradFD", n), outs):
             assert rel_err(o[idx], ref[nm]) < 1e-9, (name, N, nm)
         del keep
+
+
+@pytest.mark.parametrize("name", ["chain7", "quad12"])
+def test_large_joint_angles(name):
+    """The thread-per-knot fp64 kernels evaluate the joints' sin/cos side by
+    side (rbd_sincos_batch: two-part pi/2 reduction up to |q| = 2^20, the
+    libdevice fallback beyond): angles across both ranges, and exact
+    multiples of pi/2, match the oracle (numpy sin/cos) at 1e-9."""
+    m = models.load(name)
+    n = m.n_dof
+    N = 8448  # above ws_max_n: the thread-per-knot kernel
+    rng = np.random.default_rng(11)
+    mag = 10.0 ** rng.uniform(-3, 7.5, (N, n))  # 1e-3 .. 3e7 rad, both sides of 2^20
+    q = mag * rng.choice([-1.0, 1.0], (N, n))
+    q[:64] = (np.pi / 2) * rng.integers(-2000, 2000, (64, n))  # reduction edge cases
+    qd, tau = rng.uniform(-1, 1, (N, n)), rng.uniform(-1, 1, (N, n))
+    got = _device_eval(m, "gradFD", "f64", q, qd, tau)
+    idx = np.concatenate([np.arange(64), rng.integers(64, N, 64)])
+    ref = R.evaluate_batch(m, "gradFD", q[idx], qd[idx], tau[idx])
+    for nm in ("dq_out", "dqd_out", "qdd_out"):
+        assert rel_err(got[nm][idx].reshape(len(idx), -1), ref[nm]) < TOL["f64"], (name, nm)
