@@ -814,6 +814,7 @@ TUNING_DEFAULT = {
     "batch_sincos": True,  # thread, fp64: the joints' sin/cos evaluated side by side
                            # (rbd_sincos_batch) instead of one libdevice sincos per joint:
                            # chain7 gradFD 2^20 1.097 -> 1.081 ms, quad12 444 -> 440 us
+    "ws_fast_sincos": False,  # ws / fs: each warp's joint sin/cos by rbd_sincos_batch<1> (fp64)
     "l2_prefetch": 0,    # thread: each CTA bulk-prefetches (TMA) the input slabs of the CTA this many
                          # waves (148 SMs x MINB CTAs) ahead into L2 (0: off)
 }
@@ -1995,11 +1996,12 @@ def _ws_struct(model, alg, dt, warps, name=None, trees=None, zero_fill=True, fex
         "  typedef " + OT + " out_t;",
         "  __device__ __forceinline__ static void prologue(T* s_in, int warp, int lane) {",
     ]
+    sc_fn = "rbd_sincos_fast" if tuning(model, alg, dt).get("ws_fast_sincos") else "rbd_sincos"
     k = 0
     for op in em.ops:
         if op[0] == "sincos":
             slot = op[3]
-            src.append(f"    if (warp == {k % warps}) {{ T s, c; rbd_sincos(s_in[{slot * 33} + lane], &s, &c); "
+            src.append(f"    if (warp == {k % warps}) {{ T s, c; {sc_fn}(s_in[{slot * 33} + lane], &s, &c); "
                        f"s_in[{(em.in_total + 2 * k) * 33} + lane] = s; s_in[{(em.in_total + 2 * k + 1) * 33} + lane] = c; }}")
             k += 1
     src.append("    (void)s_in; (void)warp; (void)lane;")
@@ -2104,11 +2106,12 @@ def _fs_struct(model, alg, dt, warps, variants, name, fext=False, em=None):
             "  static constexpr int MINB = 1;",
             f"  typedef {OT} out_t;",
             "  __device__ __forceinline__ static void prologue(T* s_in, int warp, int lane) {"]
+    sc_fn = "rbd_sincos_fast" if tuning(model, alg, dt).get("ws_fast_sincos") else "rbd_sincos"
     k = 0
     for op in em.ops:
         if op[0] == "sincos":
             slot = op[3]
-            src.append(f"    if (warp == {k % warps}) {{ T s, c; rbd_sincos(s_in[{slot * 33} + lane], &s, &c); "
+            src.append(f"    if (warp == {k % warps}) {{ T s, c; {sc_fn}(s_in[{slot * 33} + lane], &s, &c); "
                        f"s_in[{(em.in_total + 2 * k) * 33} + lane] = s; s_in[{(em.in_total + 2 * k + 1) * 33} + lane] = c; }}")
             k += 1
     src += ["    (void)s_in; (void)warp; (void)lane;", "  }",

@@ -117,6 +117,9 @@ RBD_HD void rbd_sincos_batch(const double* x, double* s, double* c) {
 #endif
 }
 
+RBD_HD void rbd_sincos_fast(double x, double* s, double* c) { rbd_sincos_batch<1>(&x, s, c); }
+RBD_HD void rbd_sincos_fast(float x, float* s, float* c) { rbd_sincos(x, s, c); }
+
 RBD_HD double rbd_fma(double a, double b, double c) { return fma(a, b, c); }
 RBD_HD float rbd_fma(float a, float b, float c) { return fmaf(a, b, c); }
 
