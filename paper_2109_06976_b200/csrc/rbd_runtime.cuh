@@ -276,6 +276,56 @@ __device__ __forceinline__ void rbd_write_back(T* dst, int nk, int tid, F get) {
   }
 }
 
+// write-back through an element map (element e of a knot's output row ->
+// slot map[e] of that knot's staged row, or -1 for a structural 0).  With
+// 16-byte vectors, thread t's vectors start at elements (VW t + i NT VW)
+// mod E, which repeat with period P = lcm(NT VW, E) / (NT VW) in i: the
+// thread reads its P x VW map entries once into registers instead of one
+// shared-memory map load per element (quad12 fp32: P = 9; gradFD 2^20
+// 341 -> 328 us, gradID 300 -> 291).  Falls back to the
+// per-element form when the period is long or vectors do not tile a row.
+RBD_HDC constexpr int rbd_gcd(int a, int b) { return b == 0 ? a : rbd_gcd(b, a % b); }
+template <class T, int E, int NT>
+__device__ __forceinline__ void rbd_write_back_map(T* dst, int nk, int tid, const short* map, const T* rows,
+                                                   int stride) {
+  constexpr int VW = 16 / (int)sizeof(T);
+  constexpr int STEP = NT * VW;
+  constexpr int P = E / rbd_gcd(STEP, E);  // lcm(STEP, E) / STEP
+  if constexpr (E % VW == 0 && P * VW <= 40) {
+    if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+      short m[P][VW];
+#pragma unroll
+      for (int r = 0; r < P; ++r) {
+        const int e0 = (tid * VW + r * STEP) % E;
+#pragma unroll
+        for (int j = 0; j < VW; ++j) m[r][j] = map[e0 + j];
+      }
+      typedef typename rbd_vec16<T>::t V;
+      V* vd = reinterpret_cast<V*>(dst);
+      const int nv = nk * (E / VW);
+      for (int i0 = 0; i0 * NT < nv; i0 += P) {
+#pragma unroll
+        for (int r = 0; r < P; ++r) {
+          const int p = tid + (i0 + r) * NT;
+          if (p < nv) {
+            const int k = (p * VW) / E;
+            V v;
+            T* pv = reinterpret_cast<T*>(&v);
+#pragma unroll
+            for (int j = 0; j < VW; ++j) pv[j] = m[r][j] >= 0 ? rows[k * stride + m[r][j]] : T(0);
+            __stcs(vd + p, v);
+          }
+        }
+      }
+      return;
+    }
+  }
+  rbd_write_back<T, E, NT>(dst, nk, tid, [=](int k, int e) {
+    const int sl = map[e];
+    return sl >= 0 ? rows[k * stride + sl] : T(0);
+  });
+}
+
 template <class K>
 __global__ void __launch_bounds__(K::BK, K::MINB)
 rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __restrict__ qd,
@@ -378,16 +428,10 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
           __stcs(o2 + (base + k) * K::E2 + (e - K::E0 - K::E1), v);
       }
     } else {
-      auto from_map = [&](int off) {
-        return [=](int k, int e) {
-          const int sl = s_map[off + e];
-          return sl >= 0 ? s_in[k * K::SIN + sl] : T(0);
-        };
-      };
-      rbd_write_back<T, K::E0, BK>(o0 + base * K::E0, nk, tid, from_map(0));
-      if constexpr (K::E1 > 0) rbd_write_back<T, K::E1, BK>(o1 + base * K::E1, nk, tid, from_map(K::E0));
+      rbd_write_back_map<T, K::E0, BK>(o0 + base * K::E0, nk, tid, s_map, s_in, K::SIN);
+      if constexpr (K::E1 > 0) rbd_write_back_map<T, K::E1, BK>(o1 + base * K::E1, nk, tid, s_map + K::E0, s_in, K::SIN);
       if constexpr (K::E2 > 0)
-        rbd_write_back<T, K::E2, BK>(o2 + base * K::E2, nk, tid, from_map(K::E0 + K::E1));
+        rbd_write_back_map<T, K::E2, BK>(o2 + base * K::E2, nk, tid, s_map + K::E0 + K::E1, s_in, K::SIN);
     }
   } else if constexpr (rbd_bulk_traits<K>::on) {
     // array-major staging [BK][E0] | [BK][E1] | [BK][E2]: each array's CTA
@@ -424,6 +468,9 @@ rbd_batch_kernel(const typename K::T* __restrict__ q, const typename K::T* __res
           __stcs(o2 + (base + k) * K::E2 + (e - K::E0 - K::E1), v);
       }
     } else if constexpr (rbd_nzm<K>() > 0) {
+      // per-element map loads here: the register-cached map of
+      // rbd_write_back_map raises quad12 fp64's kernel from 164 to 178
+      // registers, which drops the third (TMEM-waiting) CTA per SM: 440 -> 546 us
       auto zm = [&](int off) {
         return [=](int k, int e) {
           const int j = s_zm[off + e];
