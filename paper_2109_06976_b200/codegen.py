@@ -816,7 +816,7 @@ TUNING_DEFAULT = {
                            # chain7 gradFD 2^20 1.097 -> 1.081 ms, quad12 444 -> 440 us
     "ws_fast_sincos": False,  # ws / fs: each warp's joint sin/cos by rbd_sincos_batch<1> (fp64)
     "l2_prefetch": 0,    # thread: each CTA bulk-prefetches (TMA) the input slabs of the CTA this many
-                         # waves (148 SMs x MINB CTAs) ahead into L2 (0: off)
+                         # waves (%nsmid SMs x MINB CTAs) ahead into L2 (0: off)
 }
 TUNED = {}
 # measured on B200 (N = 2^20): chain7 gradFD fp64 is compute-bound at 6 warps/SM

@@ -212,9 +212,9 @@ __device__ __forceinline__ bool rbd_bulk_store(T* dst, const T* src, int nk, int
   return ok;
 }
 
-#define RBD_SMS 148  // B200
 // TMA bulk prefetch into L2 of the input slabs of the CTA `waves` waves
-// ahead (the one that will take this SM slot): its input loads then hit L2
+// ahead (one wave = %nsmid SMs x MINB CTAs: roughly the CTA that will take
+// this SM slot): its input loads then hit L2
 // instead of waiting on HBM behind the output write stream.  One thread per
 // input array; the slab is [BK knots][ins(a)] contiguous (a part program's
 // window is inside it); the 16-byte-aligned body only (bulk-copy rule).
@@ -225,7 +225,9 @@ __device__ __forceinline__ void rbd_prefetch_slabs(const void* q, const void* qd
   if constexpr (waves > 0) {
     typedef typename K::T T;
     if (tid < K::NIN) {
-      const long long nb = (long long)blockIdx.x + (long long)waves * RBD_SMS * K::MINB;
+      unsigned nsm;
+      asm("mov.u32 %0, %%nsmid;" : "=r"(nsm));  // SMs on this GPU (148 on B200)
+      const long long nb = (long long)blockIdx.x + (long long)waves * nsm * K::MINB;
       const long long k0 = nb * K::BK;
       if (k0 < N) {
         const long long nk = N - k0 < K::BK ? N - k0 : K::BK;
