@@ -814,6 +814,7 @@ TUNING_DEFAULT = {
     "batch_sincos": True,  # thread, fp64: the joints' sin/cos evaluated side by side
                            # (rbd_sincos_batch) instead of one libdevice sincos per joint:
                            # chain7 gradFD 2^20 1.097 -> 1.081 ms, quad12 444 -> 440 us
+    "hot_consts": 0,     # thread, fp64: this many most-used table constants held in registers
     "ws_fast_sincos": False,  # ws / fs: each warp's joint sin/cos by rbd_sincos_batch<1> (fp64)
     "l2_prefetch": 0,    # thread: each CTA bulk-prefetches (TMA) the input slabs of the CTA this many
                          # waves (%nsmid SMs x MINB CTAs) ahead into L2 (0: off)
@@ -828,6 +829,10 @@ TUNED[("chain7", "gradFD", "f64")] = {"park": False, "bk": 32}
 # DRAM 1.64 -> 1.11 GB per launch for 1.06 GB compulsory); fp32 is slower
 # that way (0.56 -> 0.84 ms) and keeps the shared-memory row
 TUNED[("chain7", "gradFD", "f64")].update({"tmem_row": True, "prefetch_dist": 24, "prefetch_slack": 3})
+# the 64 most used fp64 table constants held in registers (loaded once):
+# 2^20 1.085 -> 1.069 ms, bit-identical (8 / 16 / 32 / 128: 1.085 / 1.085 /
+# 1.074 / 1.078; quad12 loses its third CTA per SM beyond 32)
+TUNED[("chain7", "gradFD", "f64")]["hot_consts"] = 64
 # the delta form of the second RNEA keeps rnea0's forces live across Minv/FD:
 # fewer ops but more spills in chain7's thread-per-knot kernels (2^20: fp64
 # 1.093 -> 1.120 ms, fp32 0.563 -> 0.606 ms); their warp-specialised kernels keep it
@@ -1089,11 +1094,14 @@ class ConstTable:
     def operand(self, x, lines, fresh):
         if not self.on or not _f64_needs_table(x):
             return _imm(x, "f64" if self.on else "f32")
+        r = fresh()
+        lines.append(f"ld.const.f64 {r}, [{self.symbol}+{8 * self.slot(x)}];")
+        return r
+
+    def slot(self, x):
         if x not in self.index:
             self.index[x] = len(self.index)
-        r = fresh()
-        lines.append(f"ld.const.f64 {r}, [{self.symbol}+{8 * self.index[x]}];")
-        return r
+        return self.index[x]
 
     def declaration(self):
         if not self.index:
@@ -1298,7 +1306,7 @@ def row_homes(em, scratch_base):
 
 
 def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None, plan=None, tslot=None,
-             trow=False, row_base=0, dense=None):
+             trow=False, row_base=0, dense=None, hot_consts=0):
     """Device backend: the op list as PTX for one inline-asm block.
 
     Operand %0 is the 32-bit shared address of the knot's input row (inputs,
@@ -1351,8 +1359,24 @@ def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None
         nreg += 1
         return f"{R}{nreg - 1}"
 
+    # the hot_consts most used table constants stay in registers for the
+    # whole program (loaded once) instead of a constant load per use
+    hot = {}
+    if hot_consts and ctab is not None and ctab.on:
+        cnt = {}
+        for op in em.ops:
+            if op[0] in ("fma", "mul", "add", "sub"):
+                for a in op[2:]:
+                    if isinstance(a, float) and _f64_needs_table(a):
+                        cnt[a] = cnt.get(a, 0) + 1
+        for x in sorted(cnt, key=lambda v: -cnt[v])[:int(hot_consts)]:
+            hot[x] = f"%%hc{len(hot)}"
+            lines.append(f"ld.const.f64 {hot[x]}, [{ctab.symbol}+{8 * ctab.slot(x)}];")
+
     def use(a):
         if isinstance(a, float):
+            if a in hot:
+                return hot[a]
             return ctab.operand(a, lines, fresh) if ctab is not None else imm(a)
         if plan is not None:
             return f"{R}{a}"
@@ -1522,6 +1546,8 @@ def ptx_body(em, scratch_base, out_space, sync_every=0, reload_dist=0, ctab=None
         if sync_every and narith % sync_every == 0:
             lines.append("bar.sync 1;")
     head = [f".reg .{t} {R}<{nreg}>;"]
+    if hot:
+        head.append(f".reg .f64 %%hc<{len(hot)}>;")
     if tslot or trow:
         head.append(f".reg .b32 %%tl<{em.nreg}>, %%th<{em.nreg}>;")  # TMEM load staging (32-bit halves)
     if trow:
@@ -1799,7 +1825,8 @@ def _knot_struct(model, alg, dt, name=None, trees=None, zero_fill=True, fext=Fal
                                   "quadrants)")
         L["tcols"] = tmem_alloc(tc, L["bk"]) if tslot else 0
     body, sc = ptx_body(em, em.in_total, space, tn["sync_every"], tn["reload_dist"], ctab, plan, tslot=tslot,
-                        trow=bool(L.get("trow")), row_base=L["sin"] if L.get("trow") else 0, dense=L.get("dense"))
+                        trow=bool(L.get("trow")), row_base=L["sin"] if L.get("trow") else 0, dense=L.get("dense"),
+                        hot_consts=int(tn.get("hot_consts", 0)))
     ra = (f"// register budget: {plan.reloads} reloads, {plan.stores} parked values, row {L['sin']} slots, "
           f"{L['minb']} CTAs of {L['bk']} per SM" if plan is not None else "// ptxas register allocation")
     src = [
