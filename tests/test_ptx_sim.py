@@ -22,7 +22,7 @@ def _sincos_slots(em):
     return [op[3] for op in em.ops if op[0] == "sincos"]
 
 
-def run_thread(model, alg, dt, x, stage, budget=None, park=False, fext=False, trow=False):
+def run_thread(model, alg, dt, x, stage, budget=None, park=False, fext=False, trow=False, hot=0):
     em = codegen.generate_knot(model, alg, dt, fext=fext)
     n = model.n_dof
     nin = em.in_total // n
@@ -33,7 +33,9 @@ def run_thread(model, alg, dt, x, stage, budget=None, park=False, fext=False, tr
         plan = codegen.SpillPlan(em, budget, codegen.row_homes(em, nin * n), nin * n + 2 * nsc,
                                  park_outputs=park)
     lines, sc = codegen.ptx_body(em, nin * n, "shared" if stage else "global", ctab=ctab, plan=plan,
-                                 trow=trow, row_base=nin * n + 2 * nsc)
+                                 trow=trow, row_base=nin * n + 2 * nsc, hot_consts=hot)
+    if hot and dt == "f64":
+        assert any("%%hc" in ln for ln in lines)
     if trow:
         assert sum("tcgen05.ld" in ln for ln in lines) > 0 and not any("st.shared.f" in ln and "%0+" in ln
                                                                        for ln in lines)
@@ -79,7 +81,7 @@ def run_ws(model, alg, dt, x, warps, arena_space="shared", out_space="shared", f
 
 
 @pytest.mark.parametrize("name", ["pendulum2", "chain7", "tree7", "mixed5", "quad12"])
-@pytest.mark.parametrize("mapping", ["thread", "thread_ra", "thread_park", "thread_trow", "ws"])
+@pytest.mark.parametrize("mapping", ["thread", "thread_ra", "thread_park", "thread_trow", "thread_hot", "ws"])
 def test_device_ptx_matches_reference(name, mapping):
     g = golden(name)
     m = models.load(name)
@@ -95,6 +97,10 @@ def test_device_ptx_matches_reference(name, mapping):
             elif mapping == "thread_trow":
                 # the row in tensor memory (inputs copied in, spills / reloads as tcgen05.st / ld)
                 outs = run_thread(m, alg, "f64", x, stage=True, budget=12 if k == 0 else 40, trow=True)
+            elif mapping == "thread_hot":
+                # the most used table constants held in registers (hot_consts)
+                outs = run_thread(m, alg, "f64", x, stage=True, budget=12 if k == 0 else 40, trow=True,
+                                  hot=8 if k == 0 else 64)
             elif mapping == "thread_ra":
                 # tight register budgets force heavy parking / slot reuse
                 outs = run_thread(m, alg, "f64", x, stage=(k == 0), budget=12 if k == 0 else 40)
