@@ -865,6 +865,11 @@ for _a in ALGORITHMS:
         # of the CTA one wave ahead into L2: 2^20 knots gradFD fp64 557 -> 551
         # us, fp32 344 -> 341, FD fp32 91.5 -> 89.0 (tools/experiments)
         TUNED[("quad12", _a, _d)]["l2_prefetch"] = 1
+        if _d == "f32" and _a in ("gradFD", "gradID"):
+            # 128-knot CTAs for the smem-row fp32 gradients (a longer
+            # coalesced write-back per CTA): gradFD 2^20 325 -> 303 us (with
+            # 12 warps/SM), gradID 290 -> 275 us; FD / ID / Minv neutral or slower
+            TUNED[("quad12", _a, _d)].update({"bk": 128} if _a == "gradID" else {"bk": 128, "warps_per_sm": 12})
         if _d == "f64" and _a in ("gradFD", "gradID", "Minv"):
             # the knot's row in tensor memory (8 warps x 255 registers), the
             # structural zeros (cross-leg blocks) not staged but supplied by
