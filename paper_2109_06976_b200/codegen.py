@@ -911,6 +911,10 @@ for _a in ALGORITHMS:
             # (ncu r2d: column kernel long-scoreboard stalls 26.8 -> 11.3 per
             # issue, DRAM 1.32 -> 0.86 GB per 32768 knots; then fetch-bound)
             TUNED[("humanoid30", _a, _d)].update({"split_tmem": 128, "sync_every": 256})
+            if _a in ("gradFD", "gradID"):
+                # 64 most used table constants in registers: gradFD 2^18
+                # 6.86 -> 6.78 ms (128 / 256: 6.80 / 6.79)
+                TUNED[("humanoid30", _a, _d)]["hot_consts"] = 64
 
 
 def tuning(model=None, alg=None, dtype=None):
