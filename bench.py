@@ -63,7 +63,7 @@ REF_IR_FLOPS = {  # BASELINE.md §3, counted on the reference's generated IR (FM
     ("humanoid30", "gradID"): 57839, ("humanoid30", "gradFD"): 96220,
 }
 PAPER = {"chain7": "iiwa", "quad12": "HyQ", "humanoid30": "Atlas"}
-HEADLINE_PROFILE = "ncu_summary_r2w.json"  # `ncu --set full` of the current headline kernel (tools/gpu_final.sh)
+HEADLINE_PROFILE = "ncu_summary_r2x.json"  # `ncu --set full` of the current headline kernel (tools/gpu_final.sh)
 N_IN = {"ID": 3, "Minv": 1, "FD": 3, "gradID": 3, "gradFD": 3}
 
 
