@@ -818,6 +818,10 @@ TUNING_DEFAULT = {
     "ws_fast_sincos": False,  # ws / fs: each warp's joint sin/cos by rbd_sincos_batch<1> (fp64)
     "l2_prefetch": 0,    # thread: each CTA bulk-prefetches (TMA) the input slabs of the CTA this many
                          # waves (%nsmid SMs x MINB CTAs) ahead into L2 (0: off)
+    # read with .get() (absent = off): "tmem_row" (the knot's row in tensor
+    # memory), "trow_zmap" (structural zeros unstaged, element-map write-back),
+    # "trow_bk" / "trow_ctas" / "trow_stage" (TMEM-row CTA shape experiments),
+    # "split*" (split gradient programs), "parts", "zero_memset", "ra_budget"
 }
 TUNED = {}
 # measured on B200 (N = 2^20): chain7 gradFD fp64 is compute-bound at 6 warps/SM
@@ -1616,7 +1620,9 @@ def _layout(model, alg, dt, em, device=True, over=None):
         # memory, one TMEM lane per thread (2 columns per fp64): 4-warp CTAs,
         # 2 per SM (8 warps, 255 registers), each CTA 256 columns; shared
         # memory only stages the inputs and then, aliased over them, the
-        # outputs in element order for the coalesced write-back
+        # outputs in element order for the coalesced write-back (with
+        # trow_zmap only the non-zero ones: a third CTA then fits the shared
+        # memory and waits in tcgen05.alloc with its inputs staged)
         tbk = int(tn.get("trow_bk", 128))  # 256: one 8-warp CTA per SM (all warps on one TMEM allocation)
         # CTAs per SM: 2 (255 registers, 256 TMEM columns per thread); 3-4
         # with per-thread global output stores (no output staging; 170 / 128
